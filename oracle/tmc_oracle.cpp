@@ -1,0 +1,285 @@
+// TMC ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, fp64 CPU implementation of the Tensor Monte Carlo estimator
+// (arXiv 1806.08593) and its gradient, used ONLY by tests/, by
+// __graft_entry__.smoke() and by bench.py's cpu_baseline / --impl reference
+// leg.  It shares no code, header, table or helper with the CUDA path
+// (paper_1806_08593_b200/csrc, include/tmc.h) and neither imports the other.
+//
+// What it computes (PAPER.md line numbers, "P:n"):
+//   * factor   logf_i[a,r] = log P(z_i^a | z_pa^r) - log Q(z_i^a)          P:571-576 (Appendix, typical factors)
+//              with P(z_i|z_pa) = N(mu_i(z_pa), diag exp(logvar_i(z_pa)))   P:365-369 (§Computational costs)
+//   * estimate log P_TMC = log (1/prod K_i) sum_{k_1..k_n} prod_j f_j        P:136-140 (Eq. is)
+//              evaluated by variable elimination (sum/product swap)        P:316-331 (§Efficient averaging)
+//              with one 1/K_i per eliminated index
+//              and a joint-max logsumexp (P:661-677 logmmexp is the
+//              matrix case; its separate x_i / y_k maxima are replaced by the joint max).
+//   * gradient d log P_TMC / d logf_i = pair marginal of (k_i, k_pa) under the
+//              normalised weights (autodiff of P:332 derived by marginals), then
+//              the chain rule through the Gaussian density (direct form).
+// Every routine is a literal loop over the definitions; there is no blocking,
+// fusion or reordering.  Parity pins: tests/test_oracle.py.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <vector>
+#include <algorithm>
+
+namespace {
+
+const double kNegInf = -std::numeric_limits<double>::infinity();
+const double kLog2Pi = std::log(2.0 * M_PI);
+
+// log sum_j exp(x_j) with the joint max M = max_j x_j; M = -inf => -inf.
+double lse(const std::vector<double>& x) {
+  double M = kNegInf;
+  for (double v : x) M = std::max(M, v);
+  if (M == kNegInf) return kNegInf;
+  if (std::isinf(M)) return M;  // +inf
+  double s = 0.0;
+  for (double v : x) s += std::exp(v - M);
+  return M + std::log(s);
+}
+
+// softmax_j(x_j); all -inf => all zeros (probability-zero slice).
+std::vector<double> softmax(const std::vector<double>& x) {
+  std::vector<double> p(x.size(), 0.0);
+  double L = lse(x);
+  if (L == kNegInf) return p;
+  for (size_t j = 0; j < x.size(); ++j) p[j] = std::exp(x[j] - L);
+  return p;
+}
+
+struct Graph {
+  int n, B;
+  const int *parent, *K, *D;
+  int Kp(int i) const { return parent[i] < 0 ? 1 : K[parent[i]]; }
+};
+
+struct Inputs {
+  const float *const *z, *const *mu, *const *logvar, *const *logq, *const *logobs, *const *logf_dense;
+};
+
+struct Outputs {
+  double* logp;
+  double *const *pair, *const *dz, *const *dmu, *const *dlogvar, *const *dlogq, *const *dlogobs;
+  const double* dlogp;
+};
+
+// Direct-form log density of one pair: sum_d log N(z_d; mu_d, exp(v_d)).
+double log_normal_pair(const float* z, const float* mu, const float* v, int D) {
+  double s = 0.0;
+  for (int d = 0; d < D; ++d) {
+    double zz = z[d], mm = mu[d], vv = v[d];
+    double diff = zz - mm;
+    s += -0.5 * (diff * diff * std::exp(-vv) + vv + kLog2Pi);
+  }
+  return s;
+}
+
+// logf_i[a][r] for datapoint b: P:573-576 factor = P(z_i^a | z_pa^r) / Q(z_i^a).
+std::vector<double> factor(const Graph& g, const Inputs& in, int i, int b) {
+  const int Ki = g.K[i], Kp = g.Kp(i), D = g.D[i];
+  std::vector<double> f((size_t)Ki * Kp);
+  if (in.logf_dense) {
+    const float* src = in.logf_dense[i] + (size_t)b * Ki * Kp;
+    for (size_t j = 0; j < f.size(); ++j) f[j] = src[j];
+    return f;
+  }
+  const float* z = in.z[i] + (size_t)b * Ki * D;
+  const float* mu = in.mu[i] + (size_t)b * Kp * D;
+  const float* v = in.logvar[i] + (size_t)b * Kp * D;
+  const float* lq = in.logq[i] + (size_t)b * Ki;
+  for (int a = 0; a < Ki; ++a)
+    for (int r = 0; r < Kp; ++r)
+      f[(size_t)a * Kp + r] = log_normal_pair(z + (size_t)a * D, mu + (size_t)r * D, v + (size_t)r * D, D)
+                              - (double)lq[a];
+  return f;
+}
+
+double obs(const Inputs& in, const Graph& g, int i, int b, int a) {
+  if (!in.logobs || !in.logobs[i]) return 0.0;
+  return in.logobs[i][(size_t)b * g.K[i] + a];
+}
+
+// One datapoint: upward elimination (leaves -> roots), optional downward pass
+// (chains, the north_star recursion), marginals top-down, gradients.
+void run_datapoint(const Graph& g, const Inputs& in, const Outputs& out, int direction, int b) {
+  const int n = g.n;
+  std::vector<std::vector<double>> f(n), h(n), msg(n);
+  for (int i = 0; i < n; ++i) f[i] = factor(g, in, i, b);
+
+  // O3: upward elimination, reverse topological order (parent[i] < i).
+  for (int i = 0; i < n; ++i) {
+    h[i].assign(g.K[i], 0.0);
+    for (int a = 0; a < g.K[i]; ++a) h[i][a] = obs(in, g, i, b, a);
+  }
+  double L_up = 0.0;
+  for (int i = n - 1; i >= 0; --i) {
+    const int Ki = g.K[i], Kp = g.Kp(i);
+    msg[i].assign(Kp, 0.0);
+    for (int r = 0; r < Kp; ++r) {
+      std::vector<double> t(Ki);
+      for (int a = 0; a < Ki; ++a) t[a] = f[i][(size_t)a * Kp + r] + h[i][a];
+      msg[i][r] = lse(t) - std::log((double)Ki);   // (1/K_i) sum_{k_i}
+    }
+    if (g.parent[i] >= 0) {
+      for (int r = 0; r < Kp; ++r) h[g.parent[i]][r] += msg[i][r];
+    } else {
+      L_up += msg[i][0];
+    }
+  }
+  double L = L_up;
+
+  // O3': downward recursion m_i[a] = obs_i[a] + LSE_c(logf_i[a,c] + m_p[c]) - ln K_p (chains).
+  if (direction == 1) {
+    std::vector<double> m;
+    for (int i = 0; i < n; ++i) {
+      const int Ki = g.K[i], Kp = g.Kp(i);
+      std::vector<double> mi(Ki);
+      for (int a = 0; a < Ki; ++a) {
+        std::vector<double> t(Kp);
+        for (int c = 0; c < Kp; ++c) t[c] = f[i][(size_t)a * Kp + c] + (i == 0 ? 0.0 : m[c]);
+        mi[a] = obs(in, g, i, b, a) + lse(t) - (i == 0 ? 0.0 : std::log((double)Kp));
+      }
+      m.swap(mi);
+    }
+    L = lse(m) - std::log((double)g.K[n - 1]);
+  }
+  out.logp[b] = L;
+
+  // O4: marginals top-down.  pi_root = softmax(logf_root + h_root); for a child c of p:
+  // P_c[a,r] = pi_p[r] * softmax_a(logf_c[a,r] + h_c[a]);  pi_c[a] = sum_r P_c[a,r].
+  const double w = out.dlogp ? out.dlogp[b] : 1.0;
+  std::vector<std::vector<double>> pi(n), P(n);
+  for (int i = 0; i < n; ++i) {
+    const int Ki = g.K[i], Kp = g.Kp(i);
+    P[i].assign((size_t)Ki * Kp, 0.0);
+    pi[i].assign(Ki, 0.0);
+    for (int r = 0; r < Kp; ++r) {
+      double wr = g.parent[i] < 0 ? w : pi[g.parent[i]][r];
+      std::vector<double> t(Ki);
+      for (int a = 0; a < Ki; ++a) t[a] = f[i][(size_t)a * Kp + r] + h[i][a];
+      std::vector<double> s = softmax(t);
+      for (int a = 0; a < Ki; ++a) P[i][(size_t)a * Kp + r] = wr * s[a];
+    }
+    for (int a = 0; a < Ki; ++a)
+      for (int r = 0; r < Kp; ++r) pi[i][a] += P[i][(size_t)a * Kp + r];
+  }
+
+  // O5: gradients.  dL/dlogf_i = P_i; dL/dlogobs_i = pi_i; dL/dlogq_i = -pi_i;
+  // then d logN / d{z, mu, v} in the direct form.
+  for (int i = 0; i < n; ++i) {
+    const int Ki = g.K[i], Kp = g.Kp(i), D = g.D[i];
+    if (out.pair && out.pair[i])
+      std::memcpy(out.pair[i] + (size_t)b * Ki * Kp, P[i].data(), sizeof(double) * Ki * Kp);
+    if (out.dlogobs && out.dlogobs[i])
+      for (int a = 0; a < Ki; ++a) out.dlogobs[i][(size_t)b * Ki + a] = pi[i][a];
+    if (in.logf_dense) continue;
+    if (out.dlogq && out.dlogq[i])
+      for (int a = 0; a < Ki; ++a) out.dlogq[i][(size_t)b * Ki + a] = -pi[i][a];
+    const float* z = in.z[i] + (size_t)b * Ki * D;
+    const float* mu = in.mu[i] + (size_t)b * Kp * D;
+    const float* v = in.logvar[i] + (size_t)b * Kp * D;
+    std::vector<double> dz((size_t)Ki * D, 0.0), dmu((size_t)Kp * D, 0.0), dv((size_t)Kp * D, 0.0);
+    for (int a = 0; a < Ki; ++a)
+      for (int r = 0; r < Kp; ++r) {
+        double p = P[i][(size_t)a * Kp + r];
+        if (p == 0.0) continue;
+        for (int d = 0; d < D; ++d) {
+          double zz = z[(size_t)a * D + d], mm = mu[(size_t)r * D + d], vv = v[(size_t)r * D + d];
+          double lam = std::exp(-vv), diff = zz - mm;
+          dz[(size_t)a * D + d] += p * (-diff * lam);                 // d/dz   logN = -(z-mu)/s2
+          dmu[(size_t)r * D + d] += p * (diff * lam);                 // d/dmu  logN =  (z-mu)/s2
+          dv[(size_t)r * D + d] += p * 0.5 * (diff * diff * lam - 1.0);  // d/dv logN
+        }
+      }
+    if (out.dz && out.dz[i]) std::memcpy(out.dz[i] + (size_t)b * Ki * D, dz.data(), sizeof(double) * Ki * D);
+    if (out.dmu && out.dmu[i]) std::memcpy(out.dmu[i] + (size_t)b * Kp * D, dmu.data(), sizeof(double) * Kp * D);
+    if (out.dlogvar && out.dlogvar[i])
+      std::memcpy(out.dlogvar[i] + (size_t)b * Kp * D, dv.data(), sizeof(double) * Kp * D);
+  }
+}
+
+bool valid_graph(int n, int B, const int* parent, const int* K, const int* D) {
+  if (n <= 0 || B < 0 || !parent || !K || !D) return false;
+  for (int i = 0; i < n; ++i) {
+    if (K[i] <= 0 || D[i] <= 0) return false;
+    if (parent[i] >= i || parent[i] < -1) return false;
+  }
+  return true;
+}
+
+bool is_chain(int n, const int* parent) {
+  for (int i = 0; i < n; ++i)
+    if (parent[i] != i - 1) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Joint-max logsumexp of x[0..n).  Returns -inf for n == 0.
+double or_logsumexp(const double* x, int64_t n) {
+  std::vector<double> v(x, x + n);
+  return lse(v);
+}
+
+// Z[i][k] = log sum_j exp(X[i][j] + Y[j][k])  (P:661-677 logmmexp; joint max, A2).
+int or_logmmexp(const double* X, const double* Y, int64_t I, int64_t J, int64_t Kk, double* Z) {
+  for (int64_t i = 0; i < I; ++i)
+    for (int64_t k = 0; k < Kk; ++k) {
+      std::vector<double> t(J);
+      for (int64_t j = 0; j < J; ++j) t[j] = X[i * J + j] + Y[j * Kk + k];
+      Z[i * Kk + k] = lse(t);
+    }
+  return 0;
+}
+
+// logf_i[b][a][r] (fp64) of the typical directed factorisation.
+int or_factor(int n, int B, const int* parent, const int* K, const int* D, int i,
+              const float* z, const float* mu, const float* logvar, const float* logq, double* logf) {
+  if (!valid_graph(n, B, parent, K, D) || i < 0 || i >= n) return -1;
+  Graph g{n, B, parent, K, D};
+  std::vector<const float*> zz(n, nullptr), mm(n, nullptr), vv(n, nullptr), qq(n, nullptr);
+  zz[i] = z; mm[i] = mu; vv[i] = logvar; qq[i] = logq;
+  Inputs in{zz.data(), mm.data(), vv.data(), qq.data(), nullptr, nullptr};
+  const size_t sz = (size_t)K[i] * g.Kp(i);
+  for (int b = 0; b < B; ++b) {
+    std::vector<double> f = factor(g, in, i, b);
+    std::memcpy(logf + b * sz, f.data(), sizeof(double) * sz);
+  }
+  return 0;
+}
+
+// Full estimator + gradient.  direction: 1 = downward recursion (chains only), 2 = upward.
+// Any output pointer array (or entry) may be NULL.  Returns 0, or -1 bad graph, -2 down on non-chain.
+int or_estimate(int n, int B, const int* parent, const int* K, const int* D,
+                const float* const* z, const float* const* mu, const float* const* logvar,
+                const float* const* logq, const float* const* logobs, const float* const* logf_dense,
+                int direction, const double* dlogp, double* logp,
+                double* const* pair, double* const* dz, double* const* dmu, double* const* dlogvar,
+                double* const* dlogq, double* const* dlogobs, int nthreads) {
+  if (!valid_graph(n, B, parent, K, D) || !logp) return -1;
+  if (direction == 1 && !is_chain(n, parent)) return -2;
+  Graph g{n, B, parent, K, D};
+  Inputs in{z, mu, logvar, logq, logobs, logf_dense};
+  Outputs out{logp, pair, dz, dmu, dlogvar, dlogq, dlogobs, dlogp};
+  if (nthreads <= 1 || B <= 1) {
+    for (int b = 0; b < B; ++b) run_datapoint(g, in, out, direction, b);
+    return 0;
+  }
+  nthreads = std::min(nthreads, B);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back([&, t]() {
+      for (int b = t; b < B; b += nthreads) run_datapoint(g, in, out, direction, b);
+    });
+  for (auto& x : th) x.join();
+  return 0;
+}
+
+}  // extern "C"
