@@ -1,0 +1,153 @@
+/*
+ * tmc.h — C ABI of libtmc, the B200 (sm_100a) Tensor Monte Carlo hot path.
+ *
+ * Paper: L. Aitchison, "Tensor Monte Carlo: particle methods for the GPU era",
+ * arXiv 1806.08593.  Citations "P:n" are PAPER.md line numbers.
+ *
+ * WHAT IS COMPUTED
+ *   A directed model over latents z_0..z_{n-1} whose parent structure is a tree
+ *   or forest (parent[i] < i, -1 = root).  Every latent i carries K_i proposal
+ *   samples z_i^{k}.  The conditional P(z_i | z_pa) is a
+ *   diagonal Gaussian N(mu_i(z_pa), diag exp(logvar_i(z_pa))),
+ *   evaluated by the caller at every parent sample (the root's "parent" is a
+ *   single prior, K_p = 1).  The typical factorisation gives one
+ *   pairwise factor per latent,
+ *       logf_i[b,a,c] = log N(z_i^a ; mu_i[b,c], exp(logvar_i[b,c])) - logq_i[b,a]
+ *   and observation factors logobs_i[b,a] = log P(x | z_i^a).  The TMC estimate
+ *   (Eq. is; Eq. fac) for datapoint b is
+ *       logp[b] = log( (1/prod_i K_i) * sum_{k_0..k_{n-1}} prod_i f_i * prod_i obs_i ),
+ *   evaluated by sum/product swapping as a chain/tree of log-domain
+ *   tensor inner products, never by enumeration:
+ *     DOWN (chains, the north_star recursion):
+ *       m_i[a] = logobs_i[a] + LSE_c( logf_i[a,c] + m_{i-1}[c] ) - ln K_{i-1}
+ *       logp   = LSE_a m_{n-1}[a] - ln K_{n-1}
+ *     UP (trees, leaves -> roots):
+ *       msg_{i->p}[r] = LSE_a( logf_i[a,r] + logobs_i[a] + sum_{j child of i} msg_{j->i}[a] ) - ln K_i
+ *       logp   = sum over roots of msg_{root}[0]
+ *   Non-factorised proposals (Eq. 2) enter through logq_i, which is
+ *   indexed only by k_i.  The reverse pass returns the gradient of
+ *   J = sum_b dlogp[b] * logp[b] w.r.t. every input, and optionally the pair
+ *   marginals dJ/dlogf_i[b,a,c].
+ *
+ * CONVENTIONS (all calls)
+ *   - Graph metadata (tmc_graph.parent/K/D, the pointer arrays themselves) are
+ *     HOST memory.  Every float/double buffer is DEVICE memory owned by the
+ *     caller, contiguous row-major, 4-byte aligned (16-byte for the tensor-core
+ *     path, see TMC_PREC_TC).  The library allocates nothing.
+ *   - Calls are asynchronous and stream-ordered on `stream`; they are reentrant
+ *     across streams given distinct workspaces.  Shape/graph/argument errors
+ *     are detected synchronously and nothing is launched.  Launch failures
+ *     return TMC_ERR_CUDA.  No C++ exception crosses this boundary.
+ *   - -inf is allowed in logq/logobs/logf (probability-zero event).  A
+ *     datapoint whose every tuple is impossible gets logp = -inf and all-zero
+ *     gradients (never NaN).  NaN inputs are not checked unless TMC_FLAG_VALIDATE.
+ *   - Outputs are deterministic: identical inputs give bit-identical outputs,
+ *     independent of batch position (no atomics on the data path).
+ */
+#ifndef TMC_H_
+#define TMC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t; NULL = legacy default stream. */
+typedef struct CUstream_st *tmc_stream_t;
+
+typedef enum {
+  TMC_OK = 0,
+  TMC_ERR_INVALID_ARG = -1,        /* NULL where a buffer is required, bad enum value      */
+  TMC_ERR_SHAPE = -2,              /* n<=0, B<0, K_i<=0, D_i<=0, i out of range            */
+  TMC_ERR_GRAPH = -3,              /* parent[i] >= i or < -1; DOWN requested on a non-chain */
+  TMC_ERR_ALIGNMENT = -4,          /* buffer misaligned for the requested precision path   */
+  TMC_ERR_WORKSPACE = -5,          /* ws NULL or ws_bytes < tmc_workspace_size()           */
+  TMC_ERR_UNSUPPORTED_DEVICE = -6, /* current device is not compute capability 10.0       */
+  TMC_ERR_CUDA = -7,               /* a kernel launch failed (message in tmc_last_error)   */
+  TMC_ERR_NONFINITE = -8           /* TMC_FLAG_VALIDATE found NaN/+inf in an input         */
+} tmc_status;
+
+typedef enum { TMC_DIR_AUTO = 0, TMC_DIR_DOWN = 1, TMC_DIR_UP = 2 } tmc_direction;
+/* AUTO = DOWN for chains (parent[i] == i-1), UP otherwise. Both give the same logp. */
+
+typedef enum {
+  TMC_PREC_AUTO = 0, /* TC where the shape allows it, SIMT otherwise                         */
+  TMC_PREC_SIMT = 1, /* fp32 CUDA-core direct form sum_d (z-mu)^2/s^2                        */
+  TMC_PREC_TC = 2    /* expanded quadratic form on tcgen05 tensor cores, 3-term fp16 split  */
+} tmc_precision;
+
+enum { TMC_FLAG_VALIDATE = 1u };
+
+typedef struct {
+  int32_t n;              /* number of latent variables, >= 1                                 */
+  int32_t B;              /* number of datapoints (independent problems), >= 0                */
+  const int32_t *parent;  /* HOST [n]: parent index, -1 for a root, parent[i] < i             */
+  const int32_t *K;       /* HOST [n]: samples per latent K_i >= 1                      */
+  const int32_t *D;       /* HOST [n]: dimension of latent i, >= 1                             */
+  int32_t direction;      /* tmc_direction                                                    */
+  int32_t precision;      /* tmc_precision                                                    */
+  uint32_t flags;         /* TMC_FLAG_*                                                       */
+} tmc_graph;
+
+/* Per-latent inputs (DEVICE).  K_p = K[parent[i]], or 1 for a root (its prior).             */
+typedef struct {
+  const float *z;       /* [B][K_i][D_i]  proposal samples z_i^k                               */
+  const float *mu;      /* [B][K_p][D_i]  mean of P(z_i | z_pa^c) for every parent sample c    */
+  const float *logvar;  /* [B][K_p][D_i]  log-variance of the same conditional                */
+  const float *logq;    /* [B][K_i]       log Q(z_i^k | ...)  (ignored on the dense path)      */
+  const float *logobs;  /* [B][K_i] or NULL (= 0): log P(x_i | z_i^k) of attached observations */
+} tmc_latent_in;
+
+/* Per-latent gradient outputs (DEVICE, overwritten).  Any pointer may be NULL (not wanted). */
+typedef struct {
+  float *dz;            /* [B][K_i][D_i]                                                     */
+  float *dmu;           /* [B][K_p][D_i]                                                     */
+  float *dlogvar;       /* [B][K_p][D_i]                                                     */
+  float *dlogq;         /* [B][K_i]   = -pi_i (marginal of k_i under the normalised weights) */
+  float *dlogobs;       /* [B][K_i]   =  pi_i                                                */
+  float *pair_marginal; /* [B][K_i][K_p] = dJ/dlogf_i; O(K^2) memory, small K only    */
+} tmc_latent_grad;
+
+/* Bytes of device workspace tmc_forward/tmc_backward/tmc_estimate need for this graph.
+ * Returns 0 if the graph is invalid (see tmc_last_error). */
+size_t tmc_workspace_size(const tmc_graph *g);
+
+/* Materialise the pairwise log-factor of latent i:
+ *   logf[b][a][c] = sum_d log N(z_i[b,a,d]; mu_i[b,c,d], exp(logvar_i[b,c,d])) - logq_i[b,a]
+ * logf is DEVICE [B][K_i][K_p] fp32.  O(B K_i K_p) HBM writes: for inspection/export; the
+ * estimator never materialises it. */
+tmc_status tmc_factors(const tmc_graph *g, int32_t i, const tmc_latent_in *in_i, float *logf,
+                       tmc_stream_t stream);
+
+/* Forward pass: logp[b] (DEVICE fp64 [B]).  in = HOST array of n tmc_latent_in.
+ * logf_dense: NULL for the fused Gaussian path, else a HOST array of n DEVICE pointers
+ * logf_i [B][K_i][K_p] (already containing -logq); then only in[i].logobs is read.
+ * ws/ws_bytes: device workspace; it holds the state tmc_backward needs. */
+tmc_status tmc_forward(const tmc_graph *g, const tmc_latent_in *in, const float *const *logf_dense,
+                       double *logp, void *ws, size_t ws_bytes, tmc_stream_t stream);
+
+/* Reverse pass for J = sum_b dlogp[b] logp[b] (dlogp DEVICE fp64 [B], NULL = all ones).
+ * Requires the workspace of a tmc_forward on the same graph/inputs, earlier on `stream`.
+ * out = HOST array of n tmc_latent_grad.  On the dense path dlogf_dense (HOST array of n
+ * DEVICE pointers, entries may be NULL) receives dJ/dlogf_i, and dz/dmu/dlogvar/dlogq are
+ * not written. */
+tmc_status tmc_backward(const tmc_graph *g, const tmc_latent_in *in, const float *const *logf_dense,
+                        void *ws, size_t ws_bytes, const double *dlogp, tmc_latent_grad *out,
+                        float *const *dlogf_dense, tmc_stream_t stream);
+
+/* tmc_forward + tmc_backward on the fused Gaussian path. */
+tmc_status tmc_estimate(const tmc_graph *g, const tmc_latent_in *in, double *logp, const double *dlogp,
+                        tmc_latent_grad *out, void *ws, size_t ws_bytes, tmc_stream_t stream);
+
+/* Thread-local message describing the last non-OK status on this thread. */
+const char *tmc_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t tmc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TMC_H_ */

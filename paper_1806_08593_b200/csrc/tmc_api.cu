@@ -1,0 +1,491 @@
+// libtmc host side: validation, workspace plan, and the launch schedule of the TMC message pass.
+// The ABI is declared (and documented) in include/tmc.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tmc.h"
+#include "tmc_internal.h"
+#include "tmc_simt.cuh"
+#include "tmc_tc.cuh"
+
+namespace tmc {
+namespace {
+
+thread_local std::string g_err;
+
+tmc_status fail(tmc_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+// ------------------------------------------------------------------------------------ plan
+struct EdgeBuf {
+  int R = 0, C = 0;
+  size_t out = 0, ell = 0, cbmax = 0, off = 0, h = 0, hoff = 0, w = 0, colsum = 0;
+};
+
+struct Plan {
+  int n = 0, B = 0, dir = 0, prec = 0;
+  bool dense = false;
+  std::vector<int> parent, K, D, Kp;
+  std::vector<std::vector<int>> children;
+  std::vector<int> roots;
+  std::vector<EdgeBuf> e;
+  std::vector<size_t> u, uoff;
+  size_t zero = 0, lse = 0, flag = 0;
+  std::vector<TcLatentBuf> tc;   // tensor-core operand buffers (per latent), empty for SIMT
+  size_t total = 0;
+};
+
+size_t carve(size_t& cur, size_t bytes) {
+  size_t at = (cur + 255) & ~size_t(255);
+  cur = at + bytes;
+  return at;
+}
+
+bool is_chain(const std::vector<int>& parent) {
+  for (size_t i = 0; i < parent.size(); ++i)
+    if (parent[i] != (int)i - 1) return false;
+  return true;
+}
+
+tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
+  if (!g) return fail(TMC_ERR_INVALID_ARG, "graph is NULL");
+  if (g->n <= 0) return fail(TMC_ERR_SHAPE, "n must be >= 1");
+  if (g->B < 0) return fail(TMC_ERR_SHAPE, "B must be >= 0");
+  if (!g->parent || !g->K || !g->D) return fail(TMC_ERR_INVALID_ARG, "graph parent/K/D arrays must be non-NULL");
+  if (g->direction < 0 || g->direction > 2) return fail(TMC_ERR_INVALID_ARG, "bad direction");
+  if (g->precision < 0 || g->precision > 2) return fail(TMC_ERR_INVALID_ARG, "bad precision");
+  p.n = g->n;
+  p.B = g->B;
+  p.dense = dense;
+  p.parent.assign(g->parent, g->parent + g->n);
+  p.K.assign(g->K, g->K + g->n);
+  p.D.assign(g->D, g->D + g->n);
+  p.children.assign(p.n, {});
+  for (int i = 0; i < p.n; ++i) {
+    if (p.K[i] <= 0) return fail(TMC_ERR_SHAPE, "K[" + std::to_string(i) + "] must be >= 1");
+    if (p.D[i] <= 0) return fail(TMC_ERR_SHAPE, "D[" + std::to_string(i) + "] must be >= 1");
+    if (!dense && p.D[i] > 256 && g->precision != TMC_PREC_TC)
+      return fail(TMC_ERR_SHAPE, "SIMT path supports D <= 256");
+    if (p.parent[i] < -1 || p.parent[i] >= i)
+      return fail(TMC_ERR_GRAPH, "parent[" + std::to_string(i) + "] must satisfy -1 <= parent[i] < i");
+    if (p.parent[i] >= 0) p.children[p.parent[i]].push_back(i);
+    else p.roots.push_back(i);
+  }
+  if ((int)p.roots.size() > kMaxRoots) return fail(TMC_ERR_GRAPH, "too many roots");
+  p.Kp.resize(p.n);
+  for (int i = 0; i < p.n; ++i) p.Kp[i] = p.parent[i] < 0 ? 1 : p.K[p.parent[i]];
+  const bool chain = is_chain(p.parent);
+  p.dir = g->direction == TMC_DIR_AUTO ? (chain ? TMC_DIR_DOWN : TMC_DIR_UP) : g->direction;
+  if (p.dir == TMC_DIR_DOWN && !chain) return fail(TMC_ERR_GRAPH, "TMC_DIR_DOWN requires a chain (parent[i] == i-1)");
+  // precision
+  p.prec = TMC_PREC_SIMT;
+  if (!dense && g->precision != TMC_PREC_SIMT) {
+    bool ok = tc_supported(p.parent, p.K, p.D);
+    if (g->precision == TMC_PREC_TC && !ok)
+      return fail(TMC_ERR_SHAPE, "TMC_PREC_TC needs D_i in {16,32,48,64} on every latent and K >= 1");
+    if (ok) p.prec = TMC_PREC_TC;
+  }
+
+  const size_t B = (size_t)std::max(p.B, 1);
+  size_t cur = 0;
+  p.e.resize(p.n);
+  p.u.resize(p.n);
+  p.uoff.resize(p.n);
+  for (int i = 0; i < p.n; ++i) {
+    p.u[i] = carve(cur, 4 * B * p.K[i]);
+    p.uoff[i] = carve(cur, 8 * B);
+  }
+  for (int i = 0; i < p.n; ++i) {
+    EdgeBuf& e = p.e[i];
+    if (p.dir == TMC_DIR_DOWN) { e.R = p.K[i]; e.C = p.Kp[i]; }
+    else { e.R = p.Kp[i]; e.C = p.K[i]; }
+    e.out = carve(cur, 4 * B * e.R);
+    e.ell = carve(cur, 4 * B * e.R);
+    e.cbmax = carve(cur, 4 * B);
+    e.off = carve(cur, 8 * B);
+    e.w = carve(cur, 4 * B * e.R);
+    e.colsum = carve(cur, 4 * B * e.C);
+    if (p.dir == TMC_DIR_UP) {
+      e.h = carve(cur, 4 * B * e.C);
+      e.hoff = carve(cur, 8 * B);
+    }
+  }
+  p.zero = carve(cur, 4 * B);
+  p.lse = carve(cur, 4 * B);
+  p.flag = carve(cur, 16);
+  if (p.prec == TMC_PREC_TC) tc_plan(p.parent, p.K, p.D, p.Kp, p.B, p.dir, cur, p.tc);
+  p.total = (cur + 255) & ~size_t(255);
+  return TMC_OK;
+}
+
+// ------------------------------------------------------------------------------------ device
+tmc_status check_device() {
+  static int cached[64];
+  static std::once_flag once;
+  std::call_once(once, [] { for (int& c : cached) c = -1; });
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(TMC_ERR_UNSUPPORTED_DEVICE, "no CUDA device");
+  if (dev < 0 || dev >= 64) return fail(TMC_ERR_UNSUPPORTED_DEVICE, "device index out of range");
+  if (cached[dev] < 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached[dev] = major * 10 + minor;
+  }
+  if (cached[dev] != 100)
+    return fail(TMC_ERR_UNSUPPORTED_DEVICE, "libtmc is built for sm_100a (B200); device cc = " +
+                                                std::to_string(cached[dev] / 10) + "." + std::to_string(cached[dev] % 10));
+  return TMC_OK;
+}
+
+tmc_status launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TMC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TMC_OK;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
+
+// ------------------------------------------------------------------------------------ SIMT pass dispatch
+template <bool ZR, int MODE, bool DENSE, int MAXDL>
+void launch_pass_t(const PassArgs& a, cudaStream_t s) {
+  const int NO = (MODE != 2) ? a.R : a.C;
+  const size_t smem = simt::pass_smem_bytes(a.D, DENSE);
+  auto kern = simt::pass_kernel<ZR, MODE, DENSE, MAXDL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid((NO + simt::kOPC - 1) / simt::kOPC, a.B);
+  kern<<<grid, simt::kThreads, smem, s>>>(a);
+}
+
+template <bool ZR, int MODE>
+void launch_pass_m(const PassArgs& a, bool dense, cudaStream_t s) {
+  if (dense) return launch_pass_t<ZR, MODE, true, 1>(a, s);
+  if (a.D <= 32) return launch_pass_t<ZR, MODE, false, 1>(a, s);
+  if (a.D <= 64) return launch_pass_t<ZR, MODE, false, 2>(a, s);
+  if (a.D <= 128) return launch_pass_t<ZR, MODE, false, 4>(a, s);
+  return launch_pass_t<ZR, MODE, false, 8>(a, s);
+}
+
+void launch_pass(const PassArgs& a, bool zrows, int mode, bool dense, cudaStream_t s) {
+  if (a.B == 0) return;
+  if (zrows) {
+    if (mode == 0) launch_pass_m<true, 0>(a, dense, s);
+    else if (mode == 1) launch_pass_m<true, 1>(a, dense, s);
+    else launch_pass_m<true, 2>(a, dense, s);
+  } else {
+    if (mode == 0) launch_pass_m<false, 0>(a, dense, s);
+    else if (mode == 1) launch_pass_m<false, 1>(a, dense, s);
+    else launch_pass_m<false, 2>(a, dense, s);
+  }
+}
+
+// Common PassArgs of edge i (inputs, geometry, forward state).
+PassArgs edge_args(const Plan& p, int i, const tmc_latent_in* in, const float* const* dense, void* ws) {
+  PassArgs a{};
+  const EdgeBuf& e = p.e[i];
+  a.B = p.B; a.R = e.R; a.C = e.C; a.D = p.D[i];
+  a.Kz = p.K[i]; a.Kp = p.Kp[i];
+  if (dense) a.logf = dense[i];
+  else { a.z = in[i].z; a.mu = in[i].mu; a.lv = in[i].logvar; }
+  a.cbmax = at<float>(ws, e.cbmax);
+  a.out = at<float>(ws, e.out);
+  a.ell = at<float>(ws, e.ell);
+  a.off_out = at<double>(ws, e.off);
+  if (p.dir == TMC_DIR_DOWN) {
+    const int par = p.parent[i];
+    a.cb = par < 0 ? at<float>(ws, p.zero) : at<float>(ws, p.e[par].out);
+    a.off_cb = par < 0 ? nullptr : at<double>(ws, p.e[par].off);
+    a.rb = at<float>(ws, p.u[i]);
+    a.off_rb = at<double>(ws, p.uoff[i]);
+    a.lnC = par < 0 ? 0.f : std::log((float)p.Kp[i]);
+  } else {
+    a.cb = at<float>(ws, e.h);
+    a.off_cb = at<double>(ws, e.hoff);
+    a.rb = nullptr;
+    a.off_rb = nullptr;
+    a.lnC = std::log((float)p.K[i]);
+  }
+  return a;
+}
+
+tmc_status check_inputs(const Plan& p, const tmc_latent_in* in, const float* const* dense) {
+  if (!in && !dense) return fail(TMC_ERR_INVALID_ARG, "inputs are NULL");
+  for (int i = 0; i < p.n; ++i) {
+    if (dense) {
+      if (!dense[i]) return fail(TMC_ERR_INVALID_ARG, "logf_dense[" + std::to_string(i) + "] is NULL");
+      continue;
+    }
+    if (!in[i].z || !in[i].mu || !in[i].logvar || !in[i].logq)
+      return fail(TMC_ERR_INVALID_ARG, "latent " + std::to_string(i) + ": z/mu/logvar/logq must be non-NULL");
+    if (p.prec == TMC_PREC_TC) {
+      for (const void* q : {(const void*)in[i].z, (const void*)in[i].mu, (const void*)in[i].logvar})
+        if (reinterpret_cast<uintptr_t>(q) % 16)
+          return fail(TMC_ERR_ALIGNMENT, "tensor-core path needs 16-byte aligned z/mu/logvar");
+    }
+  }
+  return TMC_OK;
+}
+
+tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* const* dense, void* ws,
+                           cudaStream_t s) {
+  int* flag = at<int>(ws, p.flag);
+  cudaMemsetAsync(flag, 0, sizeof(int), s);
+  auto scan = [&](const float* x, int64_t n, int allow) {
+    if (x && n > 0) simt::validate_kernel<<<256, 256, 0, s>>>(x, n, allow, flag);
+  };
+  const int64_t B = p.B;
+  for (int i = 0; i < p.n; ++i) {
+    if (dense) { scan(dense[i], B * p.K[i] * p.Kp[i], 1); }
+    else {
+      scan(in[i].z, B * p.K[i] * p.D[i], 0);
+      scan(in[i].mu, B * p.Kp[i] * p.D[i], 0);
+      scan(in[i].logvar, B * p.Kp[i] * p.D[i], 0);
+      scan(in[i].logq, B * p.K[i], 1);
+    }
+    if (in && in[i].logobs) scan(in[i].logobs, B * p.K[i], 1);
+  }
+  int host = 0;
+  cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return launch_check("validate");
+  if (host) return fail(TMC_ERR_NONFINITE, "NaN or +inf (or -inf in z/mu/logvar) found in an input");
+  return TMC_OK;
+}
+
+// ------------------------------------------------------------------------------------ forward
+tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* const* dense, double* logp,
+                        void* ws, cudaStream_t s) {
+  if (p.B == 0) return TMC_OK;
+  // unary prep (all latents)
+  for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
+    UnaryBatch ub{};
+    ub.B = p.B;
+    ub.count = std::min(kMaxUnaryPerLaunch, p.n - i0);
+    for (int j = 0; j < ub.count; ++j) {
+      int i = i0 + j;
+      ub.d[j].logobs = in ? in[i].logobs : nullptr;
+      ub.d[j].logq = dense ? nullptr : in[i].logq;
+      ub.d[j].u = at<float>(ws, p.u[i]);
+      ub.d[j].uoff = at<double>(ws, p.uoff[i]);
+      ub.d[j].K = p.K[i];
+    }
+    simt::unary_prep_kernel<<<dim3(p.B, ub.count), 256, 0, s>>>(ub);
+  }
+  if (p.prec == TMC_PREC_TC) {
+    tmc_status st = tc_forward(p.parent, p.K, p.D, p.Kp, p.B, p.dir, in, ws, p.tc, s);
+    if (st != TMC_OK) return st;
+  }
+  if (p.dir == TMC_DIR_DOWN) {
+    cudaMemsetAsync(at<float>(ws, p.zero), 0, 4 * (size_t)p.B, s);
+    for (int i = 0; i < p.n; ++i) {
+      PassArgs a = edge_args(p, i, in, dense, ws);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s);
+      else launch_pass(a, /*zrows=*/true, 0, dense != nullptr, s);
+    }
+    const EdgeBuf& last = p.e[p.n - 1];
+    simt::final_down_fwd_kernel<<<p.B, 256, 0, s>>>(at<float>(ws, last.out), at<double>(ws, last.off),
+                                                     p.K[p.n - 1], std::log((float)p.K[p.n - 1]),
+                                                     at<float>(ws, p.lse), logp);
+  } else {
+    for (int i = p.n - 1; i >= 0; --i) {
+      // h_i = u_i + sum of child messages
+      const std::vector<int>& ch = p.children[i];
+      int done = 0;
+      do {
+        HBuild hb{};
+        hb.B = p.B; hb.K = p.K[i];
+        hb.u = done == 0 ? at<float>(ws, p.u[i]) : at<float>(ws, p.e[i].h);
+        hb.uoff = done == 0 ? at<double>(ws, p.uoff[i]) : at<double>(ws, p.e[i].hoff);
+        hb.nchild = std::min<int>(kMaxChildren, (int)ch.size() - done);
+        for (int j = 0; j < hb.nchild; ++j) {
+          hb.msg[j] = at<float>(ws, p.e[ch[done + j]].out);
+          hb.moff[j] = at<double>(ws, p.e[ch[done + j]].off);
+        }
+        hb.h = at<float>(ws, p.e[i].h);
+        hb.hoff = at<double>(ws, p.e[i].hoff);
+        simt::hbuild_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(hb);
+        done += hb.nchild;
+      } while (done < (int)ch.size());
+      PassArgs a = edge_args(p, i, in, dense, ws);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s);
+      else launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
+    }
+    RootList rl{};
+    rl.B = p.B;
+    rl.count = (int)p.roots.size();
+    for (int j = 0; j < rl.count; ++j) {
+      rl.out[j] = at<float>(ws, p.e[p.roots[j]].out);
+      rl.off[j] = at<double>(ws, p.e[p.roots[j]].off);
+    }
+    simt::final_up_fwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, logp);
+  }
+  return launch_check("tmc_forward");
+}
+
+// ------------------------------------------------------------------------------------ backward
+tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* const* dense, void* ws,
+                         const double* dlogp, tmc_latent_grad* out, float* const* dlogf, cudaStream_t s) {
+  if (p.B == 0) return TMC_OK;
+  std::vector<const float*> pi(p.n);
+  auto grad = [&](int i) -> tmc_latent_grad { return out ? out[i] : tmc_latent_grad{}; };
+  if (p.dir == TMC_DIR_DOWN) {
+    const int L = p.n - 1;
+    simt::final_down_bwd_kernel<<<dim3((p.K[L] + 255) / 256, p.B), 256, 0, s>>>(
+        at<float>(ws, p.e[L].out), at<float>(ws, p.lse), p.K[L], dlogp, at<float>(ws, p.e[L].w));
+    for (int i = L; i >= 0; --i) {
+      PassArgs a = edge_args(p, i, in, dense, ws);
+      tmc_latent_grad g = grad(i);
+      a.w = at<float>(ws, p.e[i].w);
+      // row owner (z side): dz_i and pair marginals
+      a.gz = g.dz;
+      a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, true, 1, s);
+      else launch_pass(a, true, 1, dense != nullptr, s);
+      // column owner (param side): colsum -> w of the parent edge; dmu_i, dlogvar_i
+      a.gz = nullptr; a.pair = nullptr;
+      a.gmu = g.dmu; a.glv = g.dlogvar;
+      a.colsum = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].w) : at<float>(ws, p.e[i].colsum);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, true, 2, s);
+      else launch_pass(a, true, 2, dense != nullptr, s);
+      pi[i] = at<float>(ws, p.e[i].w);
+    }
+  } else {
+    RootList rl{};
+    rl.B = p.B;
+    rl.count = (int)p.roots.size();
+    for (int j = 0; j < rl.count; ++j) rl.w[j] = at<float>(ws, p.e[p.roots[j]].w);
+    simt::final_up_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, dlogp);
+    for (int i = 0; i < p.n; ++i) {
+      PassArgs a = edge_args(p, i, in, dense, ws);
+      tmc_latent_grad g = grad(i);
+      a.w = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].colsum) : at<float>(ws, p.e[i].w);
+      // row owner (param side): dmu_i, dlogvar_i, pair marginals
+      a.gmu = g.dmu; a.glv = g.dlogvar;
+      a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, false, 1, s);
+      else launch_pass(a, false, 1, dense != nullptr, s);
+      // column owner (z side): colsum = pi_i, dz_i
+      a.gmu = nullptr; a.glv = nullptr; a.pair = nullptr;
+      a.gz = g.dz;
+      a.colsum = at<float>(ws, p.e[i].colsum);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, false, 2, s);
+      else launch_pass(a, false, 2, dense != nullptr, s);
+      pi[i] = at<float>(ws, p.e[i].colsum);
+    }
+  }
+  for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
+    UnaryGradBatch gb{};
+    gb.B = p.B;
+    gb.count = std::min(kMaxUnaryPerLaunch, p.n - i0);
+    for (int j = 0; j < gb.count; ++j) {
+      int i = i0 + j;
+      tmc_latent_grad g = grad(i);
+      gb.d[j].pi = pi[i];
+      gb.d[j].dlogobs = g.dlogobs;
+      gb.d[j].dlogq = dense ? nullptr : g.dlogq;
+      gb.d[j].K = p.K[i];
+    }
+    simt::unary_grad_kernel<<<dim3(std::min<int64_t>(((int64_t)p.B * 64 + 255) / 256, 1024), gb.count), 256, 0, s>>>(gb);
+  }
+  return launch_check("tmc_backward");
+}
+
+}  // namespace
+}  // namespace tmc
+
+// ====================================================================================== C ABI
+using namespace tmc;
+
+extern "C" {
+
+size_t tmc_workspace_size(const tmc_graph* g) {
+  Plan p;
+  if (make_plan(g, false, p) != TMC_OK) return 0;
+  return p.total;
+}
+
+tmc_status tmc_factors(const tmc_graph* g, int32_t i, const tmc_latent_in* in_i, float* logf, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = make_plan(g, false, p);
+    if (st != TMC_OK) return st;
+    if (i < 0 || i >= p.n) return fail(TMC_ERR_SHAPE, "latent index out of range");
+    if (!in_i || !in_i->z || !in_i->mu || !in_i->logvar || !in_i->logq || !logf)
+      return fail(TMC_ERR_INVALID_ARG, "tmc_factors: NULL buffer");
+    if ((st = check_device()) != TMC_OK) return st;
+    if (p.B == 0) return TMC_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int Ki = p.K[i], Kp = p.Kp[i];
+    if (p.prec == TMC_PREC_TC && tc_factors_ok(Ki, Kp, p.D[i])) {
+      st = tc_factors(in_i, logf, p.B, Ki, Kp, p.D[i], s);
+      if (st != TMC_OK) return st;
+    } else {
+      dim3 grid((Kp + 31) / 32, (Ki + 7) / 8, p.B);
+      simt::factors_kernel<<<grid, 256, 0, s>>>(in_i->z, in_i->mu, in_i->logvar, in_i->logq, logf, Ki, Kp, p.D[i]);
+    }
+    return launch_check("tmc_factors");
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_forward(const tmc_graph* g, const tmc_latent_in* in, const float* const* logf_dense, double* logp,
+                       void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = make_plan(g, logf_dense != nullptr, p);
+    if (st != TMC_OK) return st;
+    if ((st = check_inputs(p, in, logf_dense)) != TMC_OK) return st;
+    if (!logp && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "logp is NULL");
+    if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+    if ((st = check_device()) != TMC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (g->flags & TMC_FLAG_VALIDATE)
+      if ((st = validate_inputs(p, in, logf_dense, ws, s)) != TMC_OK) return st;
+    return forward_impl(p, in, logf_dense, logp, ws, s);
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_backward(const tmc_graph* g, const tmc_latent_in* in, const float* const* logf_dense, void* ws,
+                        size_t ws_bytes, const double* dlogp, tmc_latent_grad* out, float* const* dlogf_dense,
+                        tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = make_plan(g, logf_dense != nullptr, p);
+    if (st != TMC_OK) return st;
+    if ((st = check_inputs(p, in, logf_dense)) != TMC_OK) return st;
+    if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+    if ((st = check_device()) != TMC_OK) return st;
+    return backward_impl(p, in, logf_dense, ws, dlogp, out, dlogf_dense, reinterpret_cast<cudaStream_t>(stream));
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* logp, const double* dlogp,
+                        tmc_latent_grad* out, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  tmc_status st = tmc_forward(g, in, nullptr, logp, ws, ws_bytes, stream);
+  if (st != TMC_OK) return st;
+  return tmc_backward(g, in, nullptr, ws, ws_bytes, dlogp, out, nullptr, stream);
+}
+
+const char* tmc_last_error(void) { return g_err.c_str(); }
+
+int32_t tmc_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,470 @@
+// SIMT (CUDA-core, fp32) kernels of the TMC message pass — the generic path (any K, D <= 256,
+// chains and trees, Gaussian or dense factors).  The tensor-core path (tmc_tc.cuh) replaces the
+// hot contraction for aligned shapes; these kernels remain the small-K / ragged-D path.
+//
+// One edge contraction is run as "passes" over the K_rows x K_cols pair matrix of one datapoint
+// (sum/product swap, log-domain inner product):
+//   MODE 0 (forward, row owner):   ell[r] = LSE_c(g[r,c] + cb[c] - cbmax);  out[r] = rb[r] + ell[r] - ln C
+//   MODE 1 (reverse, row owner):   P[r,c] = w[r] exp(g[r,c] + cb[c] - cbmax - ell[r]);  row-side grads
+//   MODE 2 (reverse, column owner): same P; colsum[c] = sum_r P[r,c] and column-side grads
+// P is dJ/dlogf (the pair marginal scaled by the upstream weight).  A CTA owns 32 owners
+// (rows or columns) of one datapoint, streams the other side through shared memory in chunks of 64,
+// and each warp owns 4 owners; phase 1 (lanes over streamed entries) forms g and P, phase 2 (lanes
+// over the D dimensions) accumulates the owner-side Gaussian gradients.  No atomics: every output
+// element has exactly one writer, so results are deterministic.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "tmc_internal.h"
+
+namespace tmc {
+namespace simt {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kOPW = 4;                  // owners per warp
+constexpr int kOPC = kOPW * kWarps;      // owners per CTA
+constexpr int kTC = 64;                  // streamed chunk
+
+__host__ __device__ inline int padded(int D) { return D | 1; }   // odd stride: conflict-free lanes
+
+// Dynamic shared memory bytes of pass_kernel for dimension D.
+__host__ inline size_t pass_smem_bytes(int D, bool dense) {
+  if (dense) return sizeof(float) * (4 * kTC + 4 * kOPC + kWarps * kOPW * kTC + 32);
+  int SD = padded(D);
+  size_t f = 2 * (size_t)kTC * SD + kTC      // streamed vectors (+beta)
+           + 2 * (size_t)kOPC * SD + kOPC    // owner vectors (+beta)
+           + 2 * kTC + 2 * kOPC              // scalars
+           + (size_t)kWarps * kOPW * kTC     // P buffer
+           + 32;
+  return f * sizeof(float);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// merge two (max, scaled-sum) logsumexp states
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  float M = fmaxf(m, m2);
+  if (M == -INFINITY) { m = M; s = 0.f; return; }
+  s = s * __expf(m - M) + s2 * __expf(m2 - M);
+  m = M;
+}
+
+template <bool ZROWS, int MODE, bool DENSE, int MAXDL>
+__global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
+  constexpr bool OWNER_ROW = (MODE != 2);
+  constexpr bool OWNER_Z = ZROWS ? (MODE != 2) : (MODE == 2);   // owner vectors are z-side
+  const int b = blockIdx.y;
+  const int D = a.D;
+  const int SD = padded(D);
+  const int NO = OWNER_ROW ? a.R : a.C;
+  const int NS = OWNER_ROW ? a.C : a.R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int obase = blockIdx.x * kOPC;
+
+  extern __shared__ float sm[];
+  float *sv0, *sv1, *sbeta, *ov0, *ov1, *obeta, *ss0, *ss1, *os0, *os1, *pbuf, *red;
+  {
+    float* p = sm;
+    if (!DENSE) {
+      sv0 = p; p += kTC * SD;
+      sv1 = p; p += kTC * SD;
+      sbeta = p; p += kTC;
+      ov0 = p; p += kOPC * SD;
+      ov1 = p; p += kOPC * SD;
+      obeta = p; p += kOPC;
+    } else {
+      p += 2 * kTC;  // keep layout simple
+    }
+    ss0 = p; p += kTC;
+    ss1 = p; p += kTC;
+    os0 = p; p += kOPC;
+    os1 = p; p += kOPC;
+    pbuf = p; p += kWarps * kOPW * kTC;
+    red = p;
+  }
+
+  const float* zb = DENSE ? nullptr : a.z + (int64_t)b * a.Kz * D;
+  const float* mub = DENSE ? nullptr : a.mu + (int64_t)b * a.Kp * D;
+  const float* lvb = DENSE ? nullptr : a.lv + (int64_t)b * a.Kp * D;
+  const float* cbb = a.cb + (int64_t)b * a.C;
+
+  // ---- column-bias maximum (offset pulled out of the LSE; exact in fp64 bookkeeping)
+  float cbmax;
+  if (MODE == 0) {
+    float m = -INFINITY;
+    for (int c = tid; c < a.C; c += kThreads) m = fmaxf(m, cbb[c]);
+    m = warp_max(m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (tid < 32) {
+      float v = tid < kWarps ? red[tid] : -INFINITY;
+      v = warp_max(v);
+      if (tid == 0) red[31] = (v == -INFINITY) ? 0.f : v;
+    }
+    __syncthreads();
+    cbmax = red[31];
+    if (blockIdx.x == 0 && tid == 0) {
+      a.cbmax[b] = cbmax;
+      double off = (double)cbmax;
+      if (a.off_cb) off += a.off_cb[b];
+      if (a.off_rb) off += a.off_rb[b];
+      a.off_out[b] = off;
+    }
+  } else {
+    cbmax = a.cbmax[b];
+  }
+
+  // ---- stage owner vectors and scalars
+  if (!DENSE) {
+    for (int idx = tid; idx < kOPC * D; idx += kThreads) {
+      int ol = idx / D, d = idx - ol * D, o = obase + ol;
+      float v0 = 0.f, v1 = 0.f;
+      if (o < NO) {
+        if (OWNER_Z) {
+          v0 = zb[(int64_t)o * D + d];
+        } else {
+          v0 = mub[(int64_t)o * D + d];
+          v1 = __expf(-lvb[(int64_t)o * D + d]);
+        }
+      }
+      ov0[ol * SD + d] = v0;
+      ov1[ol * SD + d] = v1;
+    }
+    if (!OWNER_Z) {
+      for (int j = 0; j < kOPW; ++j) {
+        int ol = warp * kOPW + j, o = obase + ol;
+        float s = 0.f;
+        if (o < NO)
+          for (int d = lane; d < D; d += 32) s += lvb[(int64_t)o * D + d] + kLog2Pi;
+        s = warp_sum(s);
+        if (lane == 0) obeta[ol] = -0.5f * s;
+      }
+    }
+  }
+  for (int ol = tid; ol < kOPC; ol += kThreads) {
+    int o = obase + ol;
+    float s0 = 0.f, s1 = 0.f;
+    if (o < NO) {
+      if (MODE == 1) { s0 = a.w[(int64_t)b * a.R + o]; s1 = a.ell[(int64_t)b * a.R + o]; }
+      if (MODE == 2) { s0 = cbb[o]; }
+    }
+    os0[ol] = s0;
+    os1[ol] = s1;
+  }
+
+  // per-lane state
+  float lm[kOPW], ls[kOPW], ptot[kOPW];
+  float acc0[kOPW][MAXDL], acc1[kOPW][MAXDL];
+#pragma unroll
+  for (int j = 0; j < kOPW; ++j) {
+    lm[j] = -INFINITY; ls[j] = 0.f; ptot[j] = 0.f;
+#pragma unroll
+    for (int q = 0; q < MAXDL; ++q) { acc0[j][q] = 0.f; acc1[j][q] = 0.f; }
+  }
+
+  for (int s0 = 0; s0 < NS; s0 += kTC) {
+    const int tc = min(kTC, NS - s0);
+    __syncthreads();
+    // ---- stage streamed chunk
+    if (!DENSE) {
+      for (int idx = tid; idx < tc * D; idx += kThreads) {
+        int sl = idx / D, d = idx - sl * D, s = s0 + sl;
+        if (!OWNER_Z) {   // streamed entries are z-side
+          sv0[sl * SD + d] = zb[(int64_t)s * D + d];
+        } else {
+          sv0[sl * SD + d] = mub[(int64_t)s * D + d];
+          sv1[sl * SD + d] = __expf(-lvb[(int64_t)s * D + d]);
+        }
+      }
+      if (OWNER_Z) {
+        for (int sl = warp; sl < tc; sl += kWarps) {
+          float s = 0.f;
+          for (int d = lane; d < D; d += 32) s += lvb[(int64_t)(s0 + sl) * D + d] + kLog2Pi;
+          s = warp_sum(s);
+          if (lane == 0) sbeta[sl] = -0.5f * s;
+        }
+      }
+    }
+    for (int sl = tid; sl < tc; sl += kThreads) {
+      int s = s0 + sl;
+      if (MODE == 2) { ss0[sl] = a.w[(int64_t)b * a.R + s]; ss1[sl] = a.ell[(int64_t)b * a.R + s]; }
+      else { ss0[sl] = cbb[s]; }
+    }
+    __syncthreads();
+
+    // ---- phase 1: lanes over streamed entries
+#pragma unroll
+    for (int j = 0; j < kOPW; ++j) {
+      const int ol = warp * kOPW + j, o = obase + ol;
+      if (o >= NO) continue;
+      for (int sl = lane; sl < tc; sl += 32) {
+        const int s = s0 + sl;
+        const int row = OWNER_ROW ? o : s, col = OWNER_ROW ? s : o;
+        const int ai = ZROWS ? row : col, pi = ZROWS ? col : row;
+        float g;
+        if (DENSE) {
+          g = a.logf[((int64_t)b * a.Kz + ai) * a.Kp + pi];
+        } else {
+          const float* zv = OWNER_Z ? ov0 + ol * SD : sv0 + sl * SD;
+          const float* mv = OWNER_Z ? sv0 + sl * SD : ov0 + ol * SD;
+          const float* lam = OWNER_Z ? sv1 + sl * SD : ov1 + ol * SD;
+          float q = 0.f;
+          for (int d = 0; d < D; ++d) {
+            float df = zv[d] - mv[d];
+            q = fmaf(lam[d] * df, df, q);
+          }
+          g = (OWNER_Z ? sbeta[sl] : obeta[ol]) - 0.5f * q;
+        }
+        if (MODE == 0) {
+          float x = g + ss0[sl] - cbmax;
+          if (x > lm[j]) { ls[j] = ls[j] * __expf(lm[j] - x) + 1.f; lm[j] = x; }
+          else if (x > -INFINITY) { ls[j] += __expf(x - lm[j]); }
+        } else {
+          float wr = MODE == 1 ? os0[ol] : ss0[sl];
+          float el = MODE == 1 ? os1[ol] : ss1[sl];
+          float cbv = MODE == 1 ? ss0[sl] : os0[ol];
+          float P = 0.f;
+          if (wr != 0.f && el > -INFINITY) P = wr * __expf(g + cbv - cbmax - el);
+          pbuf[(warp * kOPW + j) * kTC + sl] = P;
+          ptot[j] += P;
+          if (MODE == 1 && a.pair) a.pair[((int64_t)b * a.Kz + ai) * a.Kp + pi] = P;
+        }
+      }
+    }
+    // ---- phase 2: lanes over dimensions (owner-side Gaussian gradients)
+    if (MODE != 0 && !DENSE) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kOPW; ++j) {
+        const int ol = warp * kOPW + j, o = obase + ol;
+        if (o >= NO) continue;
+        const float* pw = pbuf + (warp * kOPW + j) * kTC;
+#pragma unroll
+        for (int q = 0; q < MAXDL; ++q) {
+          const int d = lane + 32 * q;
+          if (d >= D) continue;
+          if (OWNER_Z) {     // dz_o,d = sum_s P (mu_s,d - z_o,d) lam_s,d
+            const float zo = ov0[ol * SD + d];
+            float acc = acc0[j][q];
+            for (int sl = 0; sl < tc; ++sl) {
+              float p = pw[sl];
+              acc = fmaf(p * (sv0[sl * SD + d] - zo), sv1[sl * SD + d], acc);
+            }
+            acc0[j][q] = acc;
+          } else {           // sum_s P (z_s,d - mu_o,d) and sum_s P (z_s,d - mu_o,d)^2
+            const float mo = ov0[ol * SD + d];
+            float x0 = acc0[j][q], x1 = acc1[j][q];
+            for (int sl = 0; sl < tc; ++sl) {
+              float p = pw[sl];
+              float df = sv0[sl * SD + d] - mo;
+              float pd = p * df;
+              x0 += pd;
+              x1 = fmaf(pd, df, x1);
+            }
+            acc0[j][q] = x0; acc1[j][q] = x1;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---- epilogue
+#pragma unroll
+  for (int j = 0; j < kOPW; ++j) {
+    const int ol = warp * kOPW + j, o = obase + ol;
+    if (o >= NO) continue;   // warp-uniform
+    if (MODE == 0) {
+      float m = lm[j], s = ls[j];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+        float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+        lse_merge(m, s, m2, s2);
+      }
+      if (lane == 0) {
+        float e = (m == -INFINITY) ? -INFINITY : m + logf(s);
+        a.ell[(int64_t)b * a.R + o] = e;
+        float rbv = a.rb ? a.rb[(int64_t)b * a.R + o] : 0.f;
+        a.out[(int64_t)b * a.R + o] = rbv + e - a.lnC;
+      }
+    } else {
+      float tot = warp_sum(ptot[j]);
+      if (MODE == 2 && lane == 0 && a.colsum) a.colsum[(int64_t)b * a.C + o] = tot;
+      if (DENSE) continue;
+#pragma unroll
+      for (int q = 0; q < MAXDL; ++q) {
+        const int d = lane + 32 * q;
+        if (d >= D) continue;
+        if (OWNER_Z) {
+          if (a.gz) a.gz[((int64_t)b * a.Kz + o) * D + d] = acc0[j][q];
+        } else {
+          const float lam = ov1[ol * SD + d];
+          if (a.gmu) a.gmu[((int64_t)b * a.Kp + o) * D + d] = lam * acc0[j][q];
+          if (a.glv) a.glv[((int64_t)b * a.Kp + o) * D + d] = 0.5f * (lam * acc1[j][q] - tot);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ small kernels
+// Unary prep: u = (logobs - max logobs) - logq, uoff = max logobs (fp64 offset).
+__global__ void __launch_bounds__(256) unary_prep_kernel(const UnaryBatch ub) {
+  const UnaryDesc& d = ub.d[blockIdx.y];
+  const int b = blockIdx.x;
+  __shared__ float red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float m = 0.f;
+  if (d.logobs) {
+    m = -INFINITY;
+    for (int k = tid; k < d.K; k += 256) m = fmaxf(m, d.logobs[(int64_t)b * d.K + k]);
+    m = warp_max(m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (tid < 32) {
+      float v = tid < 8 ? red[tid] : -INFINITY;
+      v = warp_max(v);
+      if (tid == 0) red[31] = v;
+    }
+    __syncthreads();
+    m = red[31];
+  }
+  const float shift = (m == -INFINITY) ? 0.f : m;
+  for (int k = tid; k < d.K; k += 256) {
+    float v = d.logobs ? d.logobs[(int64_t)b * d.K + k] - shift : 0.f;
+    if (d.logq) v -= d.logq[(int64_t)b * d.K + k];
+    d.u[(int64_t)b * d.K + k] = v;
+  }
+  if (tid == 0) d.uoff[b] = (double)shift;
+}
+
+// h_i = u_i + sum_j msg_{j->i}  (UP direction), offsets added in fp64.
+__global__ void __launch_bounds__(256) hbuild_kernel(const HBuild h) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  if (k < h.K) {
+    float v = h.u[(int64_t)b * h.K + k];
+    for (int j = 0; j < h.nchild; ++j) v += h.msg[j][(int64_t)b * h.K + k];
+    h.h[(int64_t)b * h.K + k] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double o = h.uoff[b];
+    for (int j = 0; j < h.nchild; ++j) o += h.moff[j][b];
+    h.hoff[b] = o;
+  }
+}
+
+// DOWN final: logp = off + LSE_a m[a] - ln K; save lse for the reverse pass.
+__global__ void __launch_bounds__(256) final_down_fwd_kernel(const float* m, const double* off, int K,
+                                                             float lnK, float* lse, double* logp) {
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float red[64];
+  float mx = -INFINITY;
+  for (int k = tid; k < K; k += 256) mx = fmaxf(mx, m[(int64_t)b * K + k]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid < 32) {
+    float v = tid < 8 ? red[tid] : -INFINITY;
+    v = warp_max(v);
+    if (tid == 0) red[40] = v;
+  }
+  __syncthreads();
+  mx = red[40];
+  float s = 0.f;
+  if (mx > -INFINITY)
+    for (int k = tid; k < K; k += 256) s += __expf(m[(int64_t)b * K + k] - mx);
+  s = warp_sum(s);
+  __syncthreads();
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    float l = (mx == -INFINITY) ? -INFINITY : mx + logf(t);
+    lse[b] = l;
+    logp[b] = (l == -INFINITY) ? -INFINITY : off[b] + (double)l - (double)lnK;
+  }
+}
+
+// DOWN final reverse: w[a] = dlogp * softmax(m)[a].
+__global__ void __launch_bounds__(256) final_down_bwd_kernel(const float* m, const float* lse, int K,
+                                                             const double* dlogp, float* w) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  if (k >= K) return;
+  float l = lse[b];
+  float g = dlogp ? (float)dlogp[b] : 1.f;
+  w[(int64_t)b * K + k] = (l == -INFINITY || g == 0.f) ? 0.f : g * __expf(m[(int64_t)b * K + k] - l);
+}
+
+// UP final: logp = sum over roots of (off_root + out_root[0]).
+__global__ void final_up_fwd_kernel(const RootList r, double* logp) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= r.B) return;
+  double s = 0.0;
+  for (int j = 0; j < r.count; ++j) {
+    float o = r.out[j][b];
+    s += (o == -INFINITY) ? -INFINITY : r.off[j][b] + (double)o;
+  }
+  logp[b] = s;
+}
+
+// UP reverse seed: w_root[b] = dlogp[b]; zero if the datapoint is impossible.
+__global__ void final_up_bwd_kernel(const RootList r, const double* dlogp) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= r.B) return;
+  for (int j = 0; j < r.count; ++j) r.w[j][b] = dlogp ? (float)dlogp[b] : 1.f;
+}
+
+// dlogobs = pi, dlogq = -pi.
+__global__ void unary_grad_kernel(const UnaryGradBatch g) {
+  const UnaryGradDesc& d = g.d[blockIdx.y];
+  const int64_t n = (int64_t)g.B * d.K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float p = d.pi[i];
+    if (d.dlogobs) d.dlogobs[i] = p;
+    if (d.dlogq) d.dlogq[i] = -p;
+  }
+}
+
+// tmc_factors: logf[b][a][c] = sum_d log N(z_a; mu_c, exp v_c) - logq[a] (direct form, fp32).
+__global__ void __launch_bounds__(256) factors_kernel(const float* z, const float* mu, const float* lv,
+                                                      const float* logq, float* logf, int Ki, int Kp, int D) {
+  const int b = blockIdx.z;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int a = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (a >= Ki || c >= Kp) return;
+  const float* zv = z + ((int64_t)b * Ki + a) * D;
+  const float* mv = mu + ((int64_t)b * Kp + c) * D;
+  const float* vv = lv + ((int64_t)b * Kp + c) * D;
+  float q = 0.f, sv = 0.f;
+  for (int d = 0; d < D; ++d) {
+    float df = zv[d] - mv[d];
+    q = fmaf(__expf(-vv[d]) * df, df, q);
+    sv += vv[d] + kLog2Pi;
+  }
+  logf[((int64_t)b * Ki + a) * Kp + c] = -0.5f * (q + sv) - logq[(int64_t)b * Ki + a];
+}
+
+// TMC_FLAG_VALIDATE: flag NaN / +inf (and -inf where not allowed) in a buffer.
+__global__ void validate_kernel(const float* x, int64_t n, int allow_neginf, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = x[i];
+    bool bad = isnan(v) || v == INFINITY || (!allow_neginf && v == -INFINITY);
+    if (bad) *flag = 1;
+  }
+}
+
+}  // namespace simt
+}  // namespace tmc

@@ -1,0 +1,210 @@
+"""GPU parity: libtmc (through its C ABI) vs the fp64 oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  |logp_gpu - logp_oracle| <= 1e-3 absolute per datapoint
+  per (gradient tensor, datapoint): ||g - g*||_2 / ||g*||_2 <= 1e-3
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import tmc_workload as tw
+
+pytestmark = pytest.mark.gpu
+
+LOGP_TOL = 1e-3
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback exists)"
+    import paper_1806_08593_b200 as tmc
+    tmc.load_library()
+    return torch
+
+
+def upload(torch, wl):
+    t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return [dict(z=t(wl.z[i]), mu=t(wl.mu[i]), logvar=t(wl.logvar[i]), logq=t(wl.logq[i]), logobs=t(wl.logobs[i]))
+            for i in range(len(wl.parent))]
+
+
+def run_gpu(torch, wl, direction=0, precision=0, dlogp=None, pair=False, grads=True):
+    import paper_1806_08593_b200 as tmc
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=direction, precision=precision)
+    inp = upload(torch, wl)
+    dl = None if dlogp is None else torch.from_numpy(np.asarray(dlogp, np.float64)).cuda()
+    logp, gr = tmc.estimate(g, inp, dlogp=dl, grads=grads, pair=pair)
+    torch.cuda.synchronize()
+    out = {"logp": logp.cpu().numpy()}
+    if grads:
+        for k in gr[0]:
+            out["pair" if k == "pair_marginal" else k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
+    return out
+
+
+def rel_err(got, want):
+    """Per-datapoint relative L2 error (A16); datapoints with ||want|| < 1e-12 are skipped."""
+    errs = []
+    for b in range(want.shape[0]):
+        nw = np.linalg.norm(want[b])
+        if nw < 1e-12:
+            assert np.abs(got[b]).max() < 1e-6
+            continue
+        errs.append(np.linalg.norm(got[b] - want[b]) / nw)
+    return max(errs) if errs else 0.0
+
+
+def compare(got, ref, b_sel=None, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs"), tag=""):
+    sel = slice(None) if b_sel is None else b_sel
+    lg, lr = got["logp"][sel], ref["logp"]
+    fin = np.isfinite(lr)
+    assert np.array_equal(np.isfinite(lg), fin), tag
+    d = np.abs(lg[fin] - lr[fin])
+    assert d.max(initial=0) <= LOGP_TOL, f"{tag} max |dlogp| = {d.max()}"
+    worst = {}
+    for k in keys:
+        if k not in ref or k not in got:
+            continue
+        for i in range(len(ref[k])):
+            e = rel_err(got[k][i][sel], ref[k][i])
+            worst[(k, i)] = e
+            assert e <= GRAD_TOL, f"{tag} latent {i} {k}: rel err {e}"
+    return d.max(initial=0), worst
+
+
+# --------------------------------------------------------------------------------- small configs
+@pytest.mark.parametrize("name", ["C0", "C1", "S_chain", "S_tree", "S_mnist", "S_mlp", "S_mlp_bern"])
+@pytest.mark.parametrize("direction", ["auto", "up"])
+def test_parity_small_configs(torch_cuda, name, direction):
+    wl = tw.make_workload(name)
+    dirc = {"auto": 0, "up": 2}[direction]
+    got = run_gpu(torch_cuda, wl, direction=dirc, pair=True)
+    chain = all(p == i - 1 for i, p in enumerate(wl.parent))
+    ref = oracle.estimate_workload(wl, direction="down" if (chain and direction == "auto") else "up", pair=True)
+    compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag=name)
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("C2", dict(B=3, K=300)),            # D=64, 3 tiles of 128 + ragged tail 44
+    ("C3", dict(B=2, K=333)),            # D=32, ragged
+    ("C4", dict(B=2, K=130)),            # tree, 2 tiles + 2
+    ("C1", dict(B=5, K=37)),             # D=50/100, odd K
+])
+def test_parity_ragged_midsize(torch_cuda, name, kw):
+    wl = tw.make_workload(name, **kw)
+    got = run_gpu(torch_cuda, wl)
+    ref = oracle.estimate_workload(wl, direction="up")
+    compare(got, ref, tag=name)
+
+
+def test_dense_factor_path(torch_cuda):
+    """tmc_forward/tmc_backward with materialised logf == the fused Gaussian path."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload("C2", B=2, K=70)
+    n = len(wl.parent)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B)
+    inp = upload(torch, wl)
+    logf = [torch.empty(wl.B, wl.K[i], wl.Kp(i), device="cuda") for i in range(n)]
+    for i in range(n):
+        tmc.tmc_factors(g, i, inp[i], logf[i])
+    ref_f = [oracle.factor(wl.parent, wl.K, wl.D, i, wl.z[i], wl.mu[i], wl.logvar[i], wl.logq[i]) for i in range(n)]
+    for i in range(n):
+        np.testing.assert_allclose(logf[i].cpu().numpy(), ref_f[i], rtol=2e-5, atol=2e-3)
+    ws = tmc.alloc_workspace(g)
+    logp = torch.empty(wl.B, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward(g, inp, logp, ws, logf_dense=logf)
+    dlogf = [torch.empty_like(x) for x in logf]
+    gr = [dict(dlogobs=torch.empty(wl.B, wl.K[i], device="cuda")) for i in range(n)]
+    tmc.tmc_backward(g, inp, ws, None, gr, logf_dense=logf, dlogf_dense=dlogf)
+    torch.cuda.synchronize()
+    ref = oracle.estimate(wl.parent, wl.K, wl.D, None, None, None, None, wl.logobs,
+                          logf_dense=[x.cpu().numpy() for x in logf], pair=True)
+    got = {"logp": logp.cpu().numpy(), "pair": [x.cpu().numpy() for x in dlogf],
+           "dlogobs": [x["dlogobs"].cpu().numpy() for x in gr]}
+    compare(got, ref, keys=("pair", "dlogobs"), tag="dense")
+
+
+def test_factors_kernel_values(torch_cuda):
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    for name, kw in (("C0", {}), ("C4", dict(B=2, K=40)), ("C1", dict(B=2))):
+        wl = tw.make_workload(name, **kw)
+        g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B)
+        inp = upload(torch, wl)
+        for i in range(len(wl.parent)):
+            out = torch.empty(wl.B, wl.K[i], wl.Kp(i), device="cuda")
+            tmc.tmc_factors(g, i, inp[i], out)
+            ref = oracle.factor(wl.parent, wl.K, wl.D, i, wl.z[i], wl.mu[i], wl.logvar[i], wl.logq[i])
+            np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=2e-5, atol=2e-3)
+
+
+def test_dlogp_weights_and_zero(torch_cuda):
+    wl = tw.make_workload("C4", B=4, K=24)
+    w = np.array([1.0, -0.5, 0.0, 2.5])
+    got = run_gpu(torch_cuda, wl, dlogp=w)
+    ref = oracle.estimate_workload(wl, dlogp=w)
+    assert np.all(got["dz"][3][2] == 0.0)
+    compare(got, ref, tag="dlogp")
+
+
+def test_neg_inf_inputs(torch_cuda):
+    wl = tw.make_workload("S_chain", B=4)
+    wl.logobs[3][0, 1] = -np.inf
+    wl.logobs[3][1, :] = -np.inf
+    wl.logq[1][2, 0] = np.inf            # Q density +inf => weight 0 (logf = -inf)
+    got = run_gpu(torch_cuda, wl, pair=True)
+    ref = oracle.estimate_workload(wl, direction="down", pair=True)
+    assert got["logp"][1] == -np.inf
+    for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"):
+        for a in got[k]:
+            assert not np.isnan(a).any(), k
+            assert np.all(a[1] == 0.0), k
+    compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag="-inf")
+
+
+def test_deterministic_and_batch_position_invariant(torch_cuda):
+    wl = tw.make_workload("C4", B=6, K=40)
+    a = run_gpu(torch_cuda, wl)
+    b = run_gpu(torch_cuda, wl)
+    for k in a:
+        if k == "logp":
+            assert np.array_equal(a[k], b[k])
+        else:
+            for x, y in zip(a[k], b[k]):
+                assert np.array_equal(x, y), k
+    sub = tw.make_workload("C4", B=6, K=40, b_ids=[4, 1])   # same datapoints, other batch slots
+    c = run_gpu(torch_cuda, sub)
+    assert np.array_equal(c["logp"], a["logp"][[4, 1]])
+    assert np.array_equal(c["dz"][7], a["dz"][7][[4, 1]])
+
+
+def test_up_equals_down_on_chain(torch_cuda):
+    wl = tw.make_workload("C3", B=3, K=200)
+    d = run_gpu(torch_cuda, wl, direction=1)
+    u = run_gpu(torch_cuda, wl, direction=2)
+    assert np.abs(d["logp"] - u["logp"]).max() < 1e-3
+    for k in ("dz", "dmu", "dlogvar"):
+        for i in range(len(wl.parent)):
+            assert rel_err(d[k][i], u[k][i].astype(np.float64)) < 1e-3
+
+
+# --------------------------------------------------------------------------------- full sizes
+@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C3"])
+def test_parity_full_size_sampled(torch_cuda, name):
+    """BASELINE.json full sizes, default launch configuration (as bench.py times it); the oracle
+    recomputes a sample of datapoints one by one (inputs are keyed by global datapoint id)."""
+    cfg = tw.get_config(name)
+    wl = tw.make_workload(name)
+    got = run_gpu(torch_cuda, wl)
+    B = cfg.B
+    sample = sorted({0, 1, B // 2, B - 1})
+    sub = tw.make_workload(name, b_ids=sample)
+    ref = oracle.estimate_workload(sub, direction="up")
+    dmax, worst = compare(got, ref, b_sel=sample, tag=name)
+    print(name, "max |dlogp|", dmax, "worst grad rel", max(worst.values()))
