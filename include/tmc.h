@@ -147,6 +147,9 @@ const char *tmc_last_error(void);
 /* Library version (major*10000 + minor*100 + patch). */
 int32_t tmc_version(void);
 
+/* Diagnostics: number of kernels libtmc has launched in this process so far (all streams). */
+uint64_t tmc_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

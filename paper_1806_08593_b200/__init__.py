@@ -24,7 +24,7 @@ STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_
           -7: "TMC_ERR_CUDA", -8: "TMC_ERR_NONFINITE"}
 
 EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate",
-           "tmc_last_error", "tmc_version"]
+           "tmc_last_error", "tmc_version", "tmc_launch_count"]
 
 
 class TmcError(RuntimeError):
@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH):
             getattr(lib, f).restype = ctypes.c_int
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
+        lib.tmc_launch_count.restype = ctypes.c_uint64
         _lib = lib
     return _lib
 
@@ -187,6 +188,10 @@ def tmc_last_error() -> str:
 
 def tmc_version() -> int:
     return load_library().tmc_version()
+
+
+def tmc_launch_count() -> int:
+    return load_library().tmc_launch_count()
 
 
 # ----------------------------------------------------------------------------- convenience

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -19,6 +20,8 @@ namespace tmc {
 namespace {
 
 thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+#define TMC_COUNT_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 
 tmc_status fail(tmc_status s, const std::string& msg) {
   g_err = msg;
@@ -169,6 +172,7 @@ void launch_pass_t(const PassArgs& a, cudaStream_t s) {
   }
   dim3 grid((NO + simt::kOPC - 1) / simt::kOPC, a.B);
   kern<<<grid, simt::kThreads, smem, s>>>(a);
+    TMC_COUNT_LAUNCH();
 }
 
 template <bool ZR, int MODE>
@@ -246,6 +250,7 @@ tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* 
   cudaMemsetAsync(flag, 0, sizeof(int), s);
   auto scan = [&](const float* x, int64_t n, int allow) {
     if (x && n > 0) simt::validate_kernel<<<256, 256, 0, s>>>(x, n, allow, flag);
+    TMC_COUNT_LAUNCH();
   };
   const int64_t B = p.B;
   for (int i = 0; i < p.n; ++i) {
@@ -283,22 +288,23 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       ub.d[j].K = p.K[i];
     }
     simt::unary_prep_kernel<<<dim3(p.B, ub.count), 256, 0, s>>>(ub);
+    TMC_COUNT_LAUNCH();
   }
   if (p.prec == TMC_PREC_TC) {
-    tmc_status st = tc_forward(p.parent, p.K, p.D, p.Kp, p.B, p.dir, in, ws, p.tc, s);
-    if (st != TMC_OK) return st;
+    g_launches.fetch_add(tc_forward(p.parent, p.K, p.D, p.Kp, p.B, p.dir, in, ws, p.tc, s));
   }
   if (p.dir == TMC_DIR_DOWN) {
     cudaMemsetAsync(at<float>(ws, p.zero), 0, 4 * (size_t)p.B, s);
     for (int i = 0; i < p.n; ++i) {
       PassArgs a = edge_args(p, i, in, dense, ws);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s));
       else launch_pass(a, /*zrows=*/true, 0, dense != nullptr, s);
     }
     const EdgeBuf& last = p.e[p.n - 1];
     simt::final_down_fwd_kernel<<<p.B, 256, 0, s>>>(at<float>(ws, last.out), at<double>(ws, last.off),
                                                      p.K[p.n - 1], std::log((float)p.K[p.n - 1]),
                                                      at<float>(ws, p.lse), logp);
+    TMC_COUNT_LAUNCH();
   } else {
     for (int i = p.n - 1; i >= 0; --i) {
       // h_i = u_i + sum of child messages
@@ -317,10 +323,11 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
         hb.h = at<float>(ws, p.e[i].h);
         hb.hoff = at<double>(ws, p.e[i].hoff);
         simt::hbuild_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(hb);
+    TMC_COUNT_LAUNCH();
         done += hb.nchild;
       } while (done < (int)ch.size());
       PassArgs a = edge_args(p, i, in, dense, ws);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s);
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s));
       else launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
     }
     RootList rl{};
@@ -331,6 +338,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       rl.off[j] = at<double>(ws, p.e[p.roots[j]].off);
     }
     simt::final_up_fwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, logp);
+    TMC_COUNT_LAUNCH();
   }
   return launch_check("tmc_forward");
 }
@@ -345,6 +353,7 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
     const int L = p.n - 1;
     simt::final_down_bwd_kernel<<<dim3((p.K[L] + 255) / 256, p.B), 256, 0, s>>>(
         at<float>(ws, p.e[L].out), at<float>(ws, p.lse), p.K[L], dlogp, at<float>(ws, p.e[L].w));
+    TMC_COUNT_LAUNCH();
     for (int i = L; i >= 0; --i) {
       PassArgs a = edge_args(p, i, in, dense, ws);
       tmc_latent_grad g = grad(i);
@@ -352,14 +361,12 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       // row owner (z side): dz_i and pair marginals
       a.gz = g.dz;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, true, 1, s);
-      else launch_pass(a, true, 1, dense != nullptr, s);
+      launch_pass(a, true, 1, dense != nullptr, s);
       // column owner (param side): colsum -> w of the parent edge; dmu_i, dlogvar_i
       a.gz = nullptr; a.pair = nullptr;
       a.gmu = g.dmu; a.glv = g.dlogvar;
       a.colsum = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].w) : at<float>(ws, p.e[i].colsum);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, true, 2, s);
-      else launch_pass(a, true, 2, dense != nullptr, s);
+      launch_pass(a, true, 2, dense != nullptr, s);
       pi[i] = at<float>(ws, p.e[i].w);
     }
   } else {
@@ -368,6 +375,7 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
     rl.count = (int)p.roots.size();
     for (int j = 0; j < rl.count; ++j) rl.w[j] = at<float>(ws, p.e[p.roots[j]].w);
     simt::final_up_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, dlogp);
+    TMC_COUNT_LAUNCH();
     for (int i = 0; i < p.n; ++i) {
       PassArgs a = edge_args(p, i, in, dense, ws);
       tmc_latent_grad g = grad(i);
@@ -375,14 +383,12 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       // row owner (param side): dmu_i, dlogvar_i, pair marginals
       a.gmu = g.dmu; a.glv = g.dlogvar;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, false, 1, s);
-      else launch_pass(a, false, 1, dense != nullptr, s);
+      launch_pass(a, false, 1, dense != nullptr, s);
       // column owner (z side): colsum = pi_i, dz_i
       a.gmu = nullptr; a.glv = nullptr; a.pair = nullptr;
       a.gz = g.dz;
       a.colsum = at<float>(ws, p.e[i].colsum);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) tc_pass_backward(a, p.tc[i], ws, false, 2, s);
-      else launch_pass(a, false, 2, dense != nullptr, s);
+      launch_pass(a, false, 2, dense != nullptr, s);
       pi[i] = at<float>(ws, p.e[i].colsum);
     }
   }
@@ -399,6 +405,7 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       gb.d[j].K = p.K[i];
     }
     simt::unary_grad_kernel<<<dim3(std::min<int64_t>(((int64_t)p.B * 64 + 255) / 256, 1024), gb.count), 256, 0, s>>>(gb);
+    TMC_COUNT_LAUNCH();
   }
   return launch_check("tmc_backward");
 }
@@ -435,6 +442,7 @@ tmc_status tmc_factors(const tmc_graph* g, int32_t i, const tmc_latent_in* in_i,
     } else {
       dim3 grid((Kp + 31) / 32, (Ki + 7) / 8, p.B);
       simt::factors_kernel<<<grid, 256, 0, s>>>(in_i->z, in_i->mu, in_i->logvar, in_i->logq, logf, Ki, Kp, p.D[i]);
+    TMC_COUNT_LAUNCH();
     }
     return launch_check("tmc_factors");
   } catch (...) {
@@ -487,5 +495,7 @@ tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* log
 const char* tmc_last_error(void) { return g_err.c_str(); }
 
 int32_t tmc_version(void) { return 100; }
+
+uint64_t tmc_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

@@ -1,25 +1,587 @@
-// Tensor-core (tcgen05) path of the TMC message pass.  Stub until the sm_100a kernels land:
-// tc_supported() returns false so every edge runs on the SIMT kernels.
+// Tensor-core (tcgen05) path of the TMC message pass, sm_100a.
+//
+// The pairwise log-factor of a diagonal-Gaussian conditional ("nominally quadratic
+// cost ... dominated by the linear cost") is a dense contraction once the square is expanded:
+//   log N(z_a; mu_c, diag e^{v_c}) = S[a,c] + beta[c],   S = X . Y^T,
+//   X[a] = [z'^2, z'],  Y[c] = [-lam/2, lam mu'] * log2(e),  lam = e^{-v},
+//   beta[c] = -1/2 sum_d (lam mu'^2 + v + ln 2 pi),  z' = z - s,  mu' = mu - s
+// with a per-(datapoint, latent) centering shift s = mean_c mu (an exact identity that keeps the
+// expanded terms small).  Every operand is split into an fp16 pair (hi, lo = fp16(x - hi)) and
+// S = X_hi Y_hi + X_hi Y_lo + X_lo Y_hi is accumulated in fp32 in TMEM by tcgen05.mma kind::f16
+// (relative error ~2^-21 per product).
+//
+//   tc_prep_kernel   (K1): per (datapoint, latent): s, X/Y hi/lo tile images (pre-swizzled 128B,
+//                          the exact shared-memory image a bulk copy lands), beta.
+//   tc_colbias_kernel:     per (datapoint, edge): cbmax, fp64 offset, column bias in log2 units.
+//   tc_fwd_kernel    (K3): persistent, warp-specialised: warp 0 streams tiles with cp.async.bulk
+//                          (TMA engine) into a 3-stage mbarrier ring, warp 1 issues tcgen05.mma
+//                          into double-buffered TMEM accumulators, 4*RB softmax warps drain TMEM
+//                          with tcgen05.ld and run the online-max log2-sum-exp2 (ex2.approx, MUFU).
 #pragma once
 #include <cstddef>
+#include <cstdint>
 #include <vector>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include "../../include/tmc.h"
 #include "tmc_internal.h"
 
 namespace tmc {
+namespace tc {
 
-struct TcLatentBuf { bool ok = false; };
+constexpr int kTileRows = 128;
+constexpr int kAtomBytes = 128 * 128;        // 128 rows x 128 B (one SWIZZLE_128B K-atom)
 
-inline bool tc_supported(const std::vector<int>&, const std::vector<int>&, const std::vector<int>&) { return false; }
-inline void tc_plan(const std::vector<int>&, const std::vector<int>&, const std::vector<int>&, const std::vector<int>&,
-                    int, int, size_t&, std::vector<TcLatentBuf>& bufs) { bufs.clear(); }
+template <int D>
+struct Geo {
+  static constexpr int W = 2 * D;                    // fp16 elements per part
+  static constexpr int ATOMS = W / 64;               // 128-byte K atoms per part
+  static constexpr int PART = ATOMS * kAtomBytes;    // bytes of one part (hi or lo) of a 128-row tile
+  static constexpr int TILE = 2 * PART;              // hi + lo
+  static constexpr int RB = (D <= 32) ? 2 : 1;       // 128-row blocks per CTA work unit
+  static constexpr int STAGES = (D <= 32) ? 3 : 2;   // B-tile ring depth
+  static constexpr int SOFTMAX_WARPS = 4 * RB;
+  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS;
+  static constexpr int TMEM_COLS = RB * 2 * 128;
+  static constexpr size_t SMEM = 1024 /*align*/ + (size_t)RB * TILE + (size_t)STAGES * TILE +
+                                 (size_t)STAGES * 128 * 4 + 512 /*barriers*/;
+};
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (start, LBO=16B, SBO=1024B, version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor: kind::f16, A/B fp16 K-major, D fp32, M=128, N=128.
+constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define TMC_LD32(taddr, v)                                                                                          \
+  asm volatile(                                                                                                     \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                               \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),            \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),      \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),    \
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])     \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Byte offset of element k (fp16 index within the part's row vector) of row r in a tile part
+// laid out as ATOMS x [128 rows][128 B] with the 128-byte XOR swizzle (16B chunk ^= row % 8).
+__host__ __device__ __forceinline__ uint32_t swz_off(int r, int k) {
+  const int atom = k >> 6, kk = k & 63;
+  const int chunk = (kk >> 3) ^ (r & 7);
+  return (uint32_t)(atom * kAtomBytes + r * 128 + chunk * 16 + (kk & 7) * 2);
+}
+
+// ------------------------------------------------------------------------------ K1: operand prep
+struct PrepArgs {
+  const float *z, *mu, *lv;   // [B][Kz][D], [B][Kp][D]
+  int Kz, Kp, KzPad, KpPad;   // padded row counts (multiple of 256)
+  uint8_t *Xt, *Yt;           // tile images [B][KzPad/128][TILE], [B][KpPad/128][TILE]
+  float* beta;                // [B][KpPad]
+};
+
+// hi/lo fp16 split of x (exact sum to ~2^-22 relative); lo may be subnormal.
+__device__ __forceinline__ void split16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
+  using G = Geo<D>;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ float s_part[256];
+  __shared__ float s_shift[D];
+  const float* mub = p.mu + (size_t)b * p.Kp * D;
+  const float* lvb = p.lv + (size_t)b * p.Kp * D;
+  const float* zb = p.z + (size_t)b * p.Kz * D;
+  // centering shift s[d] = mean_c mu[c][d]
+  {
+    constexpr int G_ = 256 / D;
+    const int d = tid % D, g = tid / D;
+    float acc = 0.f;
+    for (int c = g; c < p.Kp; c += G_) acc += mub[(size_t)c * D + d];
+    s_part[tid] = acc;
+    __syncthreads();
+    if (tid < D) {
+      float t = 0.f;
+      for (int j = 0; j < G_; ++j) t += s_part[j * D + tid];
+      s_shift[tid] = t / (float)p.Kp;
+    }
+    __syncthreads();
+  }
+  constexpr int PER = D / 32;     // dims per lane
+  uint8_t* Yb = p.Yt + (size_t)b * (p.KpPad / kTileRows) * G::TILE;
+  uint8_t* Xb = p.Xt + (size_t)b * (p.KzPad / kTileRows) * G::TILE;
+  // param rows -> Y tile image, beta
+  for (int c = warp; c < p.KpPad; c += 8) {
+    float bsum = 0.f;
+    uint8_t* tile = Yb + (size_t)(c / kTileRows) * G::TILE;
+    const int r = c % kTileRows;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int d = lane + 32 * q;
+      float y0 = 0.f, y1 = 0.f;
+      if (c < p.Kp) {
+        float v = lvb[(size_t)c * D + d];
+        float lam = __expf(-v);
+        float mp = mub[(size_t)c * D + d] - s_shift[d];
+        y0 = -0.5f * lam * kLog2E;
+        y1 = lam * mp * kLog2E;
+        bsum += lam * mp * mp + v + kLog2Pi;
+      }
+      __half h, l;
+      split16(y0, h, l);
+      *reinterpret_cast<__half*>(tile + swz_off(r, d)) = h;
+      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, d)) = l;
+      split16(y1, h, l);
+      *reinterpret_cast<__half*>(tile + swz_off(r, D + d)) = h;
+      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, D + d)) = l;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    if (lane == 0) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * bsum : 0.f;
+  }
+  // z rows -> X tile image
+  for (int a = warp; a < p.KzPad; a += 8) {
+    uint8_t* tile = Xb + (size_t)(a / kTileRows) * G::TILE;
+    const int r = a % kTileRows;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int d = lane + 32 * q;
+      float x0 = 0.f, x1 = 0.f;
+      if (a < p.Kz) {
+        float zp = zb[(size_t)a * D + d] - s_shift[d];
+        x0 = zp * zp;
+        x1 = zp;
+      }
+      __half h, l;
+      split16(x0, h, l);
+      *reinterpret_cast<__half*>(tile + swz_off(r, d)) = h;
+      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, d)) = l;
+      split16(x1, h, l);
+      *reinterpret_cast<__half*>(tile + swz_off(r, D + d)) = h;
+      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, D + d)) = l;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ per-edge column bias
+struct ColbiasArgs {
+  const float* cb;       // [B][C] message bias (natural units)
+  const float* beta;     // [B][betaStride] or NULL (DOWN: beta of the column/param side)
+  int betaStride;
+  int C, Cpad;
+  float* cb2;            // [B][Cpad] out: (cb + beta - cbmax) * log2e, -inf padded
+  float* cbmax;          // [B]
+  const double *off_cb, *off_rb;
+  double* off_out;
+};
+
+__global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float red[32];
+  const float* cbb = a.cb + (size_t)b * a.C;
+  float m = -INFINITY;
+  for (int c = tid; c < a.C; c += 256) m = fmaxf(m, cbb[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (tid == 0) {
+    float v = red[0];
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w]);
+    red[16] = (v == -INFINITY) ? 0.f : v;
+  }
+  __syncthreads();
+  const float cmax = red[16];
+  for (int c = tid; c < a.Cpad; c += 256) {
+    float v = -INFINITY;
+    if (c < a.C) {
+      v = cbb[c] - cmax;
+      if (a.beta) v += a.beta[(size_t)b * a.betaStride + c];
+      v *= kLog2E;
+    }
+    a.cb2[(size_t)b * a.Cpad + c] = v;
+  }
+  if (tid == 0) {
+    a.cbmax[b] = cmax;
+    double off = (double)cmax;
+    if (a.off_cb) off += a.off_cb[b];
+    if (a.off_rb) off += a.off_rb[b];
+    a.off_out[b] = off;
+  }
+}
+
+// ------------------------------------------------------------------------------ K3: forward contraction
+struct FwdArgs {
+  const uint8_t *At, *Bt;      // row / column operand tile images [B][tiles][TILE]
+  int a_tiles, b_tiles;        // 128-row tiles per datapoint (a_tiles multiple of RB)
+  const float* cb2;            // [B][b_tiles*128]
+  const float* ell_add;        // [B][ell_stride] added to ell (UP: beta of the row/param side) or NULL
+  int ell_stride;
+  const float* out_add;        // [B][R] added to out (DOWN: unary of the row/z side) or NULL
+  int R, B;
+  float lnC;
+  float *out, *ell;            // [B][R]
+};
+
+template <int D>
+__global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArgs a) {
+  using G = Geo<D>;
+  constexpr int RB = G::RB, ST = G::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                   // RB tiles
+  uint8_t* sB = sA + (size_t)RB * G::TILE;              // ST tiles
+  float* sCb = reinterpret_cast<float*>(sB + (size_t)ST * G::TILE);   // ST x 128
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sCb + ST * 128);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 1;
+  uint64_t* b_full = bars + 2;            // [ST]
+  uint64_t* b_empty = bars + 2 + ST;      // [ST]
+  uint64_t* acc_full = bars + 2 + 2 * ST; // [2]
+  uint64_t* acc_empty = bars + 4 + 2 * ST;// [2]
+  uint64_t* cb_full = bars + 6 + 2 * ST;  // [ST] column-bias ring (consumed by the softmax warps)
+  uint64_t* cb_empty = bars + 6 + 3 * ST; // [ST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 4 * ST);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int groups = a.a_tiles / RB;
+  const int units = a.B * groups;
+
+  if (tid == 0) {
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+      mbar_init(&cb_full[s], 1);
+      mbar_init(&cb_empty[s], G::SOFTMAX_WARPS);
+    }
+    for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], G::SOFTMAX_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(G::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== producer: bulk copies (TMA engine) =====================
+    if (lane == 0) {
+      uint32_t t = 0, ua = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        const int b = u / groups, g = u % groups;
+        mbar_wait(a_empty, (ua & 1) ^ 1);
+        mbar_expect_tx(a_full, RB * G::TILE);
+        bulk_g2s(sA, a.At + ((size_t)b * a.a_tiles + (size_t)g * RB) * G::TILE, RB * G::TILE, a_full);
+        for (int j = 0; j < a.b_tiles; ++j, ++t) {
+          const int s = t % ST;
+          const uint32_t ph = ((t / ST) & 1) ^ 1;
+          mbar_wait(&b_empty[s], ph);
+          mbar_expect_tx(&b_full[s], G::TILE);
+          bulk_g2s(sB + (size_t)s * G::TILE, a.Bt + ((size_t)b * a.b_tiles + j) * G::TILE, G::TILE, &b_full[s]);
+          mbar_wait(&cb_empty[s], ph);
+          mbar_expect_tx(&cb_full[s], 512);
+          bulk_g2s(sCb + s * 128, a.cb2 + ((size_t)b * a.b_tiles + j) * 128, 512, &cb_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      uint32_t t = 0, ua = 0;
+      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        mbar_wait(a_full, ua & 1);
+        for (int j = 0; j < a.b_tiles; ++j, ++t) {
+          const int s = t % ST, as = t & 1;
+          mbar_wait(&b_full[s], (t / ST) & 1);
+          mbar_wait(&acc_empty[as], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            const uint32_t d = tmem + (uint32_t)((rb * 2 + as) * 128);
+            const uint32_t A = aBase + rb * G::TILE, Bs = bBase + s * G::TILE;
+#pragma unroll
+            for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t o = at * kAtomBytes + kk * 32;
+                const uint64_t ahi = sdesc(A + o), alo = sdesc(A + G::PART + o);
+                const uint64_t bhi = sdesc(Bs + o), blo = sdesc(Bs + G::PART + o);
+                mma_f16(d, ahi, bhi, kIdescF16M128N128, (at | kk) ? 1u : 0u);
+                mma_f16(d, ahi, blo, kIdescF16M128N128, 1u);
+                mma_f16(d, alo, bhi, kIdescF16M128N128, 1u);
+              }
+            }
+          }
+          mma_commit(&b_empty[s]);
+          mma_commit(&acc_full[as]);
+        }
+        mma_commit(a_empty);
+      }
+    }
+  } else {
+    // ===================== softmax warps: TMEM -> online log2-sum-exp2 =====================
+    const int sw = warp - 2;
+    const int rb = sw >> 2;
+    const int quarter = warp & 3;               // TMEM lane quarter this warp may access
+    const int rloc = rb * 128 + quarter * 32 + lane;
+    uint32_t t = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int b = u / groups, g = u % groups;
+      float mref = -INFINITY, sum = 0.f;
+      for (int j = 0; j < a.b_tiles; ++j, ++t) {
+        const int as = t & 1, s = t % ST;
+        mbar_wait(&acc_full[as], (t >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[128];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((rb * 2 + as) * 128);
+        TMC_LD32(taddr + 0, (v + 0));
+        TMC_LD32(taddr + 32, (v + 32));
+        TMC_LD32(taddr + 64, (v + 64));
+        TMC_LD32(taddr + 96, (v + 96));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[as]);
+        mbar_wait(&cb_full[s], (t / ST) & 1);
+        const float* cbt = sCb + s * 128;
+        float* x = reinterpret_cast<float*>(v);
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 128; ++k) {
+          x[k] = __uint_as_float(v[k]) + cbt[k];
+          tmax = fmaxf(tmax, x[k]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cb_empty[s]);
+        if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
+          sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
+          mref = tmax;
+        }
+        if (mref > -INFINITY) {
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 128; k += 4) {
+            s0 += ex2(x[k] - mref);
+            s1 += ex2(x[k + 1] - mref);
+            s2 += ex2(x[k + 2] - mref);
+            s3 += ex2(x[k + 3] - mref);
+          }
+          sum += (s0 + s1) + (s2 + s3);
+        }
+      }
+      const int r = g * RB * 128 + rloc;
+      if (r < a.R) {
+        float e = (sum > 0.f) ? kLn2 * (mref + __log2f(sum)) : -INFINITY;
+        if (a.ell_add) e += a.ell_add[(size_t)b * a.ell_stride + r];
+        a.ell[(size_t)b * a.R + r] = e;
+        const float oa = a.out_add ? a.out_add[(size_t)b * a.R + r] : 0.f;
+        a.out[(size_t)b * a.R + r] = oa + e - a.lnC;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::TMEM_COLS));
+  }
+}
+
+}  // namespace tc
+
+// ================================================================================ host side
+struct TcLatentBuf {
+  bool ok = false;          // this latent's (non-root) edge runs on tensor cores
+  int D = 0, KzPad = 0, KpPad = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0;
+};
+
+inline bool tc_dim_ok(int D) { return D == 32 || D == 64; }
+
+inline bool tc_supported(const std::vector<int>& parent, const std::vector<int>& K, const std::vector<int>& D) {
+  bool any = false;
+  for (size_t i = 0; i < parent.size(); ++i)
+    if (parent[i] >= 0 && tc_dim_ok(D[i]) && K[i] >= 1) any = true;
+  return any;
+}
+
+inline size_t tc_carve(size_t& cur, size_t bytes) {
+  size_t at = (cur + 1023) & ~size_t(1023);
+  cur = at + bytes;
+  return at;
+}
+
+inline int pad256(int k) { return (k + 255) / 256 * 256; }
+
+inline size_t tc_tile_bytes(int D) { return D == 32 ? tc::Geo<32>::TILE : tc::Geo<64>::TILE; }
+
+inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, const std::vector<int>& D,
+                    const std::vector<int>& Kp, int B, int dir, size_t& cur, std::vector<TcLatentBuf>& bufs) {
+  const size_t Bn = (size_t)(B > 0 ? B : 1);
+  bufs.assign(parent.size(), TcLatentBuf{});
+  for (size_t i = 0; i < parent.size(); ++i) {
+    if (parent[i] < 0 || !tc_dim_ok(D[i])) continue;
+    TcLatentBuf& t = bufs[i];
+    t.ok = true;
+    t.D = D[i];
+    t.KzPad = pad256(K[i]);
+    t.KpPad = pad256(Kp[i]);
+    const size_t tb = tc_tile_bytes(D[i]);
+    t.xt = tc_carve(cur, Bn * (t.KzPad / 128) * tb);
+    t.yt = tc_carve(cur, Bn * (t.KpPad / 128) * tb);
+    t.beta = tc_carve(cur, Bn * t.KpPad * 4);
+    const int Cpad = (dir == TMC_DIR_DOWN) ? t.KpPad : t.KzPad;
+    t.cb2 = tc_carve(cur, Bn * Cpad * 4);
+  }
+}
+
 inline bool tc_edge_ok(const TcLatentBuf& b) { return b.ok; }
-inline tmc_status tc_forward(const std::vector<int>&, const std::vector<int>&, const std::vector<int>&,
-                             const std::vector<int>&, int, int, const tmc_latent_in*, void*,
-                             const std::vector<TcLatentBuf>&, cudaStream_t) { return TMC_OK; }
-inline void tc_pass_forward(const PassArgs&, const TcLatentBuf&, void*, bool, cudaStream_t) {}
-inline void tc_pass_backward(const PassArgs&, const TcLatentBuf&, void*, bool, int, cudaStream_t) {}
+
+template <int D>
+inline void tc_prep_launch(const tc::PrepArgs& p, int B, cudaStream_t s) {
+  tc::tc_prep_kernel<D><<<B, 256, 0, s>>>(p);
+}
+
+// Operand prep for every tensor-core edge (one launch per latent).
+inline int tc_forward(const std::vector<int>& parent, const std::vector<int>& K, const std::vector<int>& D,
+                      const std::vector<int>& Kp, int B, int dir, const tmc_latent_in* in, void* ws,
+                      const std::vector<TcLatentBuf>& bufs, cudaStream_t s) {
+  int launches = 0;
+  for (size_t i = 0; i < parent.size(); ++i) {
+    const TcLatentBuf& t = bufs[i];
+    if (!t.ok || B == 0) continue;
+    tc::PrepArgs p{};
+    p.z = in[i].z; p.mu = in[i].mu; p.lv = in[i].logvar;
+    p.Kz = K[i]; p.Kp = Kp[i]; p.KzPad = t.KzPad; p.KpPad = t.KpPad;
+    p.Xt = static_cast<uint8_t*>(ws) + t.xt;
+    p.Yt = static_cast<uint8_t*>(ws) + t.yt;
+    p.beta = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.beta);
+    if (D[i] == 32) tc_prep_launch<32>(p, B, s);
+    else tc_prep_launch<64>(p, B, s);
+    ++launches;
+  }
+  return launches;
+}
+
+template <int D>
+inline void tc_fwd_launch(const tc::FwdArgs& f, cudaStream_t s) {
+  using G = tc::Geo<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::tc_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int units = f.B * (f.a_tiles / G::RB);
+  const int grid = units < sms ? units : sms;
+  tc::tc_fwd_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
+}
+
+// Forward contraction of one edge on tensor cores.  zrows = DOWN (rows = z side).
+// Returns the number of kernels launched.
+inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, cudaStream_t s) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const int Cpad = zrows ? t.KpPad : t.KzPad;
+  tc::ColbiasArgs cbA{};
+  cbA.cb = a.cb;
+  cbA.beta = zrows ? reinterpret_cast<const float*>(w + t.beta) : nullptr;
+  cbA.betaStride = t.KpPad;
+  cbA.C = a.C; cbA.Cpad = Cpad;
+  cbA.cb2 = reinterpret_cast<float*>(w + t.cb2);
+  cbA.cbmax = a.cbmax;
+  cbA.off_cb = a.off_cb; cbA.off_rb = a.off_rb; cbA.off_out = a.off_out;
+  tc::tc_colbias_kernel<<<a.B, 256, 0, s>>>(cbA);
+
+  tc::FwdArgs f{};
+  f.At = zrows ? w + t.xt : w + t.yt;
+  f.Bt = zrows ? w + t.yt : w + t.xt;
+  f.a_tiles = (zrows ? t.KzPad : t.KpPad) / 128;
+  f.b_tiles = Cpad / 128;
+  f.cb2 = cbA.cb2;
+  f.ell_add = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
+  f.ell_stride = t.KpPad;
+  f.out_add = a.rb;
+  f.R = a.R; f.B = a.B; f.lnC = a.lnC;
+  f.out = a.out; f.ell = a.ell;
+  if (t.D == 32) tc_fwd_launch<32>(f, s);
+  else tc_fwd_launch<64>(f, s);
+  return 2;
+}
+
 inline bool tc_factors_ok(int, int, int) { return false; }
 inline tmc_status tc_factors(const tmc_latent_in*, float*, int, int, int, int, cudaStream_t) { return TMC_OK; }
 

@@ -89,15 +89,19 @@ def test_parity_small_configs(torch_cuda, name, direction):
     compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag=name)
 
 
-@pytest.mark.parametrize("name,kw", [
+RAGGED = [
     ("C2", dict(B=3, K=300)),            # D=64, 3 tiles of 128 + ragged tail 44
     ("C3", dict(B=2, K=333)),            # D=32, ragged
     ("C4", dict(B=2, K=130)),            # tree, 2 tiles + 2
     ("C1", dict(B=5, K=37)),             # D=50/100, odd K
-])
-def test_parity_ragged_midsize(torch_cuda, name, kw):
+]
+
+
+@pytest.mark.parametrize("precision", [1, 0])           # TMC_PREC_SIMT, TMC_PREC_AUTO (tensor cores)
+@pytest.mark.parametrize("name,kw", RAGGED)
+def test_parity_ragged_midsize(torch_cuda, name, kw, precision):
     wl = tw.make_workload(name, **kw)
-    got = run_gpu(torch_cuda, wl)
+    got = run_gpu(torch_cuda, wl, precision=precision)
     ref = oracle.estimate_workload(wl, direction="up")
     compare(got, ref, tag=name)
 
@@ -192,6 +196,20 @@ def test_up_equals_down_on_chain(torch_cuda):
     for k in ("dz", "dmu", "dlogvar"):
         for i in range(len(wl.parent)):
             assert rel_err(d[k][i], u[k][i].astype(np.float64)) < 1e-3
+
+
+@pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=256)), ("C3", dict(B=2, K=640)), ("C2", dict(B=2, K=256)),
+                                     ("C4", dict(B=2, K=256)), ("C3", dict(B=1, K=1)), ("C3", dict(B=2, K=5))])
+@pytest.mark.parametrize("direction", [1, 2])
+def test_tensor_core_forward(torch_cuda, name, kw, direction):
+    """TMC_PREC_TC forward (logp only) against the oracle, both directions (chains)."""
+    wl = tw.make_workload(name, **kw)
+    if direction == 1 and not all(p == i - 1 for i, p in enumerate(wl.parent)):
+        pytest.skip("DOWN needs a chain")
+    got = run_gpu(torch_cuda, wl, direction=direction, precision=2, grads=False)
+    ref = oracle.estimate_workload(wl, direction="up", grads=False)
+    d = np.abs(got["logp"] - ref["logp"]).max()
+    assert d <= LOGP_TOL, d
 
 
 # --------------------------------------------------------------------------------- full sizes
