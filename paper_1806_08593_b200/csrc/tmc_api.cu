@@ -290,14 +290,16 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
     simt::unary_prep_kernel<<<dim3(p.B, ub.count), 256, 0, s>>>(ub);
     TMC_COUNT_LAUNCH();
   }
-  if (p.prec == TMC_PREC_TC) {
-    g_launches.fetch_add(tc_forward(p.parent, p.K, p.D, p.Kp, p.B, p.dir, in, ws, p.tc, s));
-  }
   if (p.dir == TMC_DIR_DOWN) {
     cudaMemsetAsync(at<float>(ws, p.zero), 0, 4 * (size_t)p.B, s);
     for (int i = 0; i < p.n; ++i) {
       PassArgs a = edge_args(p, i, in, dense, ws);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s));
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) {
+        // centre on the parent's filtering weights m_pa (predicted location of z_i)
+        g_launches.fetch_add(tc_prep_edge(p.K[i], p.Kp[i], p.D[i], p.B, in[i], ws, p.tc[i],
+                                          at<float>(ws, p.e[p.parent[i]].out), p.Kp[i], 0, s));
+        g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s));
+      }
       else launch_pass(a, /*zrows=*/true, 0, dense != nullptr, s);
     }
     const EdgeBuf& last = p.e[p.n - 1];
@@ -327,7 +329,12 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
         done += hb.nchild;
       } while (done < (int)ch.size());
       PassArgs a = edge_args(p, i, in, dense, ws);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s));
+      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) {
+        // centre on softmax(h_i): z_i weighted by its subtree evidence
+        g_launches.fetch_add(tc_prep_edge(p.K[i], p.Kp[i], p.D[i], p.B, in[i], ws, p.tc[i],
+                                          at<float>(ws, p.e[i].h), p.K[i], 1, s));
+        g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s));
+      }
       else launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
     }
     RootList rl{};
@@ -361,12 +368,15 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       // row owner (z side): dz_i and pair marginals
       a.gz = g.dz;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
-      launch_pass(a, true, 1, dense != nullptr, s);
+      const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 1, s));
+      else launch_pass(a, true, 1, dense != nullptr, s);
       // column owner (param side): colsum -> w of the parent edge; dmu_i, dlogvar_i
       a.gz = nullptr; a.pair = nullptr;
       a.gmu = g.dmu; a.glv = g.dlogvar;
       a.colsum = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].w) : at<float>(ws, p.e[i].colsum);
-      launch_pass(a, true, 2, dense != nullptr, s);
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 2, s));
+      else launch_pass(a, true, 2, dense != nullptr, s);
       pi[i] = at<float>(ws, p.e[i].w);
     }
   } else {
@@ -383,12 +393,15 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       // row owner (param side): dmu_i, dlogvar_i, pair marginals
       a.gmu = g.dmu; a.glv = g.dlogvar;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
-      launch_pass(a, false, 1, dense != nullptr, s);
+      const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, false, 1, s));
+      else launch_pass(a, false, 1, dense != nullptr, s);
       // column owner (z side): colsum = pi_i, dz_i
       a.gmu = nullptr; a.glv = nullptr; a.pair = nullptr;
       a.gz = g.dz;
       a.colsum = at<float>(ws, p.e[i].colsum);
-      launch_pass(a, false, 2, dense != nullptr, s);
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, false, 2, s));
+      else launch_pass(a, false, 2, dense != nullptr, s);
       pi[i] = at<float>(ws, p.e[i].colsum);
     }
   }

@@ -136,6 +136,10 @@ struct PrepArgs {
   int Kz, Kp, KzPad, KpPad;   // padded row counts (multiple of 256)
   uint8_t *Xt, *Yt;           // tile images [B][KzPad/128][TILE], [B][KpPad/128][TILE]
   float* beta;                // [B][KpPad]
+  float* shift;               // [B][D] centering shift s (the reverse pass needs z', mu')
+  const float* wsrc;          // [B][wlen] log-weights of the centering mean (messages), or NULL
+  int wlen;
+  int wz;                     // 1: s = sum_a softmax(wsrc)[a] z[a] ; 0: s = sum_c softmax(wsrc)[c] mu[c]
 };
 
 // hi/lo fp16 split of x (exact sum to ~2^-22 relative); lo may be subnormal.
@@ -154,18 +158,57 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
   const float* mub = p.mu + (size_t)b * p.Kp * D;
   const float* lvb = p.lv + (size_t)b * p.Kp * D;
   const float* zb = p.z + (size_t)b * p.Kz * D;
-  // centering shift s[d] = mean_c mu[c][d]
+  // centering shift s[d]: the posterior-weighted mean of the samples the message pass has
+  // already weighted (UP: softmax(h_i) over z_i; DOWN: softmax(m_pa) over mu_i), else mean_c mu.
+  // Any s is exact algebra; a posterior-centred s keeps the expanded terms of the pairs that carry
+  // weight small, so the fp32 tensor-core accumulator never holds large cancelling partial sums.
   {
+    __shared__ float s_w[2048 + 32];
+    const float* vec = mub;
+    int nrow = p.Kp;
+    bool weighted = false;
+    if (p.wsrc && p.wlen <= 2048) {
+      vec = p.wz ? zb : mub;
+      nrow = p.wz ? p.Kz : p.Kp;
+      const float* wb = p.wsrc + (size_t)b * p.wlen;
+      float m = -INFINITY;
+      for (int k = tid; k < nrow; k += 256) m = fmaxf(m, wb[k]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) s_part[warp] = m;
+      __syncthreads();
+      if (tid == 0) {
+        float v = s_part[0];
+        for (int w = 1; w < 8; ++w) v = fmaxf(v, s_part[w]);
+        s_w[2048] = v;
+      }
+      __syncthreads();
+      const float mx = s_w[2048];
+      weighted = mx > -INFINITY;
+      if (weighted)
+        for (int k = tid; k < nrow; k += 256) s_w[k] = __expf(wb[k] - mx);
+      __syncthreads();
+    }
     constexpr int G_ = 256 / D;
     const int d = tid % D, g = tid / D;
-    float acc = 0.f;
-    for (int c = g; c < p.Kp; c += G_) acc += mub[(size_t)c * D + d];
+    float acc = 0.f, wsum = 0.f;
+    if (weighted) {
+      for (int k = g; k < nrow; k += G_) { acc += s_w[k] * vec[(size_t)k * D + d]; wsum += s_w[k]; }
+    } else {
+      for (int c = g; c < p.Kp; c += G_) acc += mub[(size_t)c * D + d];
+      wsum = 0.f;
+    }
+    __syncthreads();
     s_part[tid] = acc;
+    __shared__ float s_ws[256];
+    s_ws[tid] = wsum;
     __syncthreads();
     if (tid < D) {
-      float t = 0.f;
-      for (int j = 0; j < G_; ++j) t += s_part[j * D + tid];
-      s_shift[tid] = t / (float)p.Kp;
+      float t = 0.f, ws = 0.f;
+      for (int j = 0; j < G_; ++j) { t += s_part[j * D + tid]; ws += s_ws[j * D]; }
+      if (!weighted) ws = (float)p.Kp;
+      s_shift[tid] = t / ws;
+      p.shift[(size_t)b * D + tid] = t / ws;
     }
     __syncthreads();
   }
@@ -368,16 +411,23 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
           for (int rb = 0; rb < RB; ++rb) {
             const uint32_t d = tmem + (uint32_t)((rb * 2 + as) * 128);
             const uint32_t A = aBase + rb * G::TILE, Bs = bBase + s * G::TILE;
+            // small cross terms first, the large hi*hi products last: fewer fp32 accumulator
+            // roundings at large partial-sum magnitude
 #pragma unroll
             for (int at = 0; at < G::ATOMS; ++at) {
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t o = at * kAtomBytes + kk * 32;
-                const uint64_t ahi = sdesc(A + o), alo = sdesc(A + G::PART + o);
-                const uint64_t bhi = sdesc(Bs + o), blo = sdesc(Bs + G::PART + o);
-                mma_f16(d, ahi, bhi, kIdescF16M128N128, (at | kk) ? 1u : 0u);
-                mma_f16(d, ahi, blo, kIdescF16M128N128, 1u);
-                mma_f16(d, alo, bhi, kIdescF16M128N128, 1u);
+                mma_f16(d, sdesc(A + o), sdesc(Bs + G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
+                mma_f16(d, sdesc(A + G::PART + o), sdesc(Bs + o), kIdescF16M128N128, 1u);
+              }
+            }
+#pragma unroll
+            for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t o = at * kAtomBytes + kk * 32;
+                mma_f16(d, sdesc(A + o), sdesc(Bs + o), kIdescF16M128N128, 1u);
               }
             }
           }
@@ -456,13 +506,322 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   }
 }
 
+
+// ------------------------------------------------------------------------------ K4: reverse pass
+// One "owner" pass of the reverse contraction.  The CTA owns 128 rows m of one
+// datapoint and streams the other side in 128-wide tiles n:
+//   P~[m,n] = ex2(S2[m,n] + ho[m] + ht[n] + 14)          (= 2^14 |w| exp(logf + bias - ell))
+//   G[m,:] += sum_n P~[m,n] T[n,:]                         (tcgen05, P~ and T both fp16 hi/lo)
+//   rowsum[m] = sum_n P~[m,n]
+// S is recomputed on tensor cores exactly as in the forward; P~ is written (swizzled, hi/lo) to
+// shared memory and is the A operand of the gradient GEMM, whose B operand is the streamed tile
+// itself read MN-major.  The epilogue turns G into dz (T = Y tiles) or dmu/dlogvar (T = X tiles).
+struct BwdArgs {
+  const uint8_t *Ot, *Tt;      // owned / streamed tile images [B][tiles][TILE]
+  int o_tiles, t_tiles;
+  const float* ho;             // [B][o_tiles*128] owned log2 term
+  const float* ht;             // [B][t_tiles*128] streamed log2 term (-inf padded)
+  const float* sgn;            // [B] sign of the upstream weights
+  int M, B;
+  int owner_z;                 // 1: G = sum P Y -> dz ; 0: G = sum P X -> dmu, dlogvar
+  const float *z, *mu, *lv;    // owner-side fp32 inputs [B][M][D]
+  const float* shift;          // [B][D]
+  float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
+  float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
+};
+
+template <int D>
+struct BGeo {
+  static constexpr int TILE = Geo<D>::TILE;
+  static constexpr int PART = Geo<D>::PART;
+  static constexpr int ATOMS = Geo<D>::ATOMS;
+  static constexpr int ST = 3;
+  static constexpr int THREADS = 192;
+  static constexpr int PBYTES = 2 * 2 * kAtomBytes;            // P~ hi + lo, 128 x 128 fp16 each
+  static constexpr int GCOL = 256;                             // TMEM column of the gradient accumulator
+  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + PBYTES + ST * 512 + 512;
+};
+
+// MN-major SWIZZLE_128B descriptor: LBO = stride of 64-element MN chunks, SBO = 8-row K groups.
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int D>
+__global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdArgs a) {
+  using G = BGeo<D>;
+  constexpr int ST = G::ST;
+  constexpr uint32_t IDESC_S = kIdescF16M128N128;
+  constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | ((uint32_t)(2 * D) >> 3 << 17) | ((128u >> 4) << 24);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sO = smem;
+  uint8_t* sT = sO + G::TILE;
+  uint8_t* sP = sT + (size_t)ST * G::TILE;
+  float* sHt = reinterpret_cast<float*>(sP + G::PBYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sHt + ST * 128);
+  uint64_t* o_full = bars + 0;
+  uint64_t* o_empty = bars + 1;
+  uint64_t* t_full = bars + 2;              // [ST]
+  uint64_t* t_empty = bars + 2 + ST;        // [ST]
+  uint64_t* h_full = bars + 2 + 2 * ST;     // [ST]
+  uint64_t* h_empty = bars + 2 + 3 * ST;    // [ST]
+  uint64_t* s_full = bars + 2 + 4 * ST;     // [2]
+  uint64_t* s_empty = bars + 4 + 4 * ST;    // [2]
+  uint64_t* p_full = bars + 6 + 4 * ST;
+  uint64_t* p_empty = bars + 7 + 4 * ST;
+  uint64_t* g_full = bars + 8 + 4 * ST;
+  uint64_t* g_empty = bars + 9 + 4 * ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 4 * ST);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int units = a.B * a.o_tiles;
+  if (tid == 0) {
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], 4);
+    }
+    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 4); }
+    mbar_init(p_full, 4); mbar_init(p_empty, 1);
+    mbar_init(g_full, 1); mbar_init(g_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- producer
+      uint32_t t = 0, ua = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        const int b = u / a.o_tiles, mt = u % a.o_tiles;
+        mbar_wait(o_empty, (ua & 1) ^ 1);
+        mbar_expect_tx(o_full, G::TILE);
+        bulk_g2s(sO, a.Ot + ((size_t)b * a.o_tiles + mt) * G::TILE, G::TILE, o_full);
+        for (int j = 0; j < a.t_tiles; ++j, ++t) {
+          const int s = t % ST;
+          const uint32_t ph = ((t / ST) & 1) ^ 1;
+          mbar_wait(&t_empty[s], ph);
+          mbar_expect_tx(&t_full[s], G::TILE);
+          bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, G::TILE, &t_full[s]);
+          mbar_wait(&h_empty[s], ph);
+          mbar_expect_tx(&h_full[s], 512);
+          bulk_g2s(sHt + s * 128, a.ht + ((size_t)b * a.t_tiles + j) * 128, 512, &h_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      uint32_t t = 0, ua = 0;
+      const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT), pBase = smem_u32(sP);
+      auto grad = [&](uint32_t tt, bool first) {
+        mbar_wait(p_full, tt & 1);
+        if (first) mbar_wait(g_empty, (ua & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t Ts = tBase + (tt % ST) * G::TILE;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t po = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+          const uint64_t phi = sdesc(pBase + po), plo = sdesc(pBase + 2 * kAtomBytes + po);
+          const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
+          mma_f16(tmem + G::GCOL, phi, thi, IDESC_G, (!first || kk) ? 1u : 0u);
+          mma_f16(tmem + G::GCOL, phi, tlo, IDESC_G, 1u);
+          mma_f16(tmem + G::GCOL, plo, thi, IDESC_G, 1u);
+        }
+        mma_commit(&t_empty[tt % ST]);
+        mma_commit(p_empty);
+      };
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        mbar_wait(o_full, ua & 1);
+        for (int j = 0; j < a.t_tiles; ++j, ++t) {
+          const int s = t % ST, as = t & 1;
+          mbar_wait(&t_full[s], (t / ST) & 1);
+          mbar_wait(&s_empty[as], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
+#pragma unroll
+          for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t o = at * kAtomBytes + kk * 32;
+              mma_f16(d, sdesc(oBase + o), sdesc(Ts + G::PART + o), IDESC_S, (at | kk) ? 1u : 0u);
+              mma_f16(d, sdesc(oBase + G::PART + o), sdesc(Ts + o), IDESC_S, 1u);
+            }
+          }
+#pragma unroll
+          for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t o = at * kAtomBytes + kk * 32;
+              mma_f16(d, sdesc(oBase + o), sdesc(Ts + o), IDESC_S, 1u);
+            }
+          }
+          mma_commit(&s_full[as]);
+          if (j > 0) grad(t - 1, j == 1);
+        }
+        grad(t - 1, a.t_tiles == 1);
+        mma_commit(g_full);
+        mma_commit(o_empty);
+      }
+    }
+  } else {
+    // ---------------- softmax / P~ producer warps (4) + epilogue
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;          // owned row within the tile
+    uint32_t t = 0, ua = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      const int b = u / a.o_tiles, mt = u % a.o_tiles;
+      const int gm = mt * 128 + m;
+      const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
+      float rsum = 0.f;
+      for (int j = 0; j < a.t_tiles; ++j, ++t) {
+        const int as = t & 1, s = t % ST;
+        mbar_wait(&s_full[as], (t >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[128];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * 128);
+        TMC_LD32(taddr + 0, (v + 0));
+        TMC_LD32(taddr + 32, (v + 32));
+        TMC_LD32(taddr + 64, (v + 64));
+        TMC_LD32(taddr + 96, (v + 96));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[as]);
+        mbar_wait(&h_full[s], (t / ST) & 1);
+        float* x = reinterpret_cast<float*>(v);
+        const float* hts = sHt + s * 128;
+        if (hom > -INFINITY) {
+#pragma unroll
+          for (int k = 0; k < 128; ++k) {
+            x[k] = ex2(__uint_as_float(v[k]) + hts[k] + hom);
+            rsum += x[k];
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 128; ++k) x[k] = 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&h_empty[s]);
+        mbar_wait(p_empty, (t & 1) ^ 1);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float p0 = x[c * 8 + 2 * q], p1 = x[c * 8 + 2 * q + 1];
+            __half2 h = __floats2half2_rn(p0, p1);
+            float2 hf = __half22float2(h);
+            __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+            hi[q] = *reinterpret_cast<uint32_t*>(&h);
+            lo[q] = *reinterpret_cast<uint32_t*>(&l);
+          }
+          const uint32_t off = swz_off(m, c * 8);
+          *reinterpret_cast<uint4*>(sP + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(sP + 2 * kAtomBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      // ---------------- epilogue: G -> gradients
+      mbar_wait(g_full, ua & 1);
+      tc_fence_after();
+      float g[2 * D];
+      {
+        uint32_t* gv = reinterpret_cast<uint32_t*>(g);
+        const uint32_t gaddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)G::GCOL;
+#pragma unroll
+        for (int c = 0; c < 2 * D / 32; ++c) TMC_LD32(gaddr + 32 * c, (gv + 32 * c));
+        tmem_ld_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(g_empty);
+      if (gm < a.M) {
+        const float sc = a.sgn[b] * (1.f / 16384.f);
+        const float pi = rsum * sc;
+        const float* sh = a.shift + (size_t)b * D;
+        const size_t row = ((size_t)b * a.M + gm) * D;
+        if (a.owner_z) {
+          // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
+          if (a.gz) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              const float zp = a.z[row + d] - sh[d];
+              a.gz[row + d] = (g[D + d] + 2.f * zp * g[d]) * (sc * kLn2);
+            }
+          }
+        } else {
+          // G = sum P (X = [z'^2, z']): A2 = sum P z'^2, A1 = sum P z'
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const float mp = a.mu[row + d] - sh[d];
+            const float lam = __expf(-a.lv[row + d]);
+            const float A1 = g[D + d] * sc, A2 = g[d] * sc;
+            if (a.gmu) a.gmu[row + d] = lam * (A1 - mp * pi);
+            if (a.glv) a.glv[row + d] = 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+          }
+        }
+        if (a.rowsum) a.rowsum[(size_t)b * a.M + gm] = pi;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Per-row terms of the reverse pass: rterm2[r] = log2|w[r]| - (ell[r] - beta[r]) log2e (-inf when
+// the row carries no weight), sgn[b] = sign of the (uniformly signed) upstream weights.
+struct RowtermArgs {
+  const float *ell, *w, *beta;   // [B][R], [B][R], [B][betaStride] (UP: beta of the row side) or NULL
+  int betaStride, R, Rpad;
+  float* rterm2;                 // [B][Rpad]
+  float* sgn;                    // [B]
+};
+
+__global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
+  const int b = blockIdx.x, tid = threadIdx.x;
+  __shared__ int neg;
+  if (tid == 0) neg = 0;
+  __syncthreads();
+  for (int r = tid; r < a.Rpad; r += 256) {
+    float v = -INFINITY;
+    if (r < a.R) {
+      const float e = a.ell[(size_t)b * a.R + r], w = a.w[(size_t)b * a.R + r];
+      if (w < 0.f) neg = 1;
+      if (e > -INFINITY && w != 0.f) {
+        const float bt = a.beta ? a.beta[(size_t)b * a.betaStride + r] : 0.f;
+        v = __log2f(fabsf(w)) - (e - bt) * kLog2E;
+      }
+    }
+    a.rterm2[(size_t)b * a.Rpad + r] = v;
+  }
+  __syncthreads();
+  if (tid == 0) a.sgn[b] = neg ? -1.f : 1.f;
+}
+
 }  // namespace tc
 
 // ================================================================================ host side
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
-  size_t xt = 0, yt = 0, beta = 0, cb2 = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, shift = 0, rterm2 = 0, sgn = 0;
+  bool bwd_ok = false;      // reverse pass on tensor cores (D == 32)
 };
 
 inline bool tc_dim_ok(int D) { return D == 32 || D == 64; }
@@ -500,7 +859,12 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     t.yt = tc_carve(cur, Bn * (t.KpPad / 128) * tb);
     t.beta = tc_carve(cur, Bn * t.KpPad * 4);
     const int Cpad = (dir == TMC_DIR_DOWN) ? t.KpPad : t.KzPad;
+    const int Rpad = (dir == TMC_DIR_DOWN) ? t.KzPad : t.KpPad;
     t.cb2 = tc_carve(cur, Bn * Cpad * 4);
+    t.shift = tc_carve(cur, Bn * D[i] * 4);
+    t.rterm2 = tc_carve(cur, Bn * Rpad * 4);
+    t.sgn = tc_carve(cur, Bn * 4);
+    t.bwd_ok = (D[i] == 32);
   }
 }
 
@@ -511,25 +875,22 @@ inline void tc_prep_launch(const tc::PrepArgs& p, int B, cudaStream_t s) {
   tc::tc_prep_kernel<D><<<B, 256, 0, s>>>(p);
 }
 
-// Operand prep for every tensor-core edge (one launch per latent).
-inline int tc_forward(const std::vector<int>& parent, const std::vector<int>& K, const std::vector<int>& D,
-                      const std::vector<int>& Kp, int B, int dir, const tmc_latent_in* in, void* ws,
-                      const std::vector<TcLatentBuf>& bufs, cudaStream_t s) {
-  int launches = 0;
-  for (size_t i = 0; i < parent.size(); ++i) {
-    const TcLatentBuf& t = bufs[i];
-    if (!t.ok || B == 0) continue;
-    tc::PrepArgs p{};
-    p.z = in[i].z; p.mu = in[i].mu; p.lv = in[i].logvar;
-    p.Kz = K[i]; p.Kp = Kp[i]; p.KzPad = t.KzPad; p.KpPad = t.KpPad;
-    p.Xt = static_cast<uint8_t*>(ws) + t.xt;
-    p.Yt = static_cast<uint8_t*>(ws) + t.yt;
-    p.beta = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.beta);
-    if (D[i] == 32) tc_prep_launch<32>(p, B, s);
-    else tc_prep_launch<64>(p, B, s);
-    ++launches;
-  }
-  return launches;
+// Operand prep of one tensor-core edge (latent i): X/Y tile images, beta and the centering shift.
+// wsrc/wlen/wz: the message weights the shift is centred on (see tc_prep_kernel).
+inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in, void* ws, const TcLatentBuf& t,
+                        const float* wsrc, int wlen, int wz, cudaStream_t s) {
+  if (!t.ok || B == 0) return 0;
+  tc::PrepArgs p{};
+  p.z = in.z; p.mu = in.mu; p.lv = in.logvar;
+  p.Kz = Ki; p.Kp = Kpi; p.KzPad = t.KzPad; p.KpPad = t.KpPad;
+  p.Xt = static_cast<uint8_t*>(ws) + t.xt;
+  p.Yt = static_cast<uint8_t*>(ws) + t.yt;
+  p.beta = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.beta);
+  p.shift = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.shift);
+  p.wsrc = wsrc; p.wlen = wlen; p.wz = wz;
+  if (Di == 32) tc_prep_launch<32>(p, B, s);
+  else tc_prep_launch<64>(p, B, s);
+  return 1;
 }
 
 template <int D>
@@ -580,6 +941,68 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   if (t.D == 32) tc_fwd_launch<32>(f, s);
   else tc_fwd_launch<64>(f, s);
   return 2;
+}
+
+template <int D>
+inline void tc_bwd_launch(const tc::BwdArgs& f, cudaStream_t s) {
+  using G = tc::BGeo<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::tc_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int units = f.B * f.o_tiles;
+  const int grid = units < sms ? units : sms;
+  tc::tc_bwd_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
+}
+
+inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.ok && t.bwd_ok && !a.pair; }
+
+// Reverse pass of one edge on tensor cores: row-owner pass (mode 1) or column-owner pass (mode 2).
+// The row terms are prepared once, before the row-owner pass.  Returns kernels launched.
+inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, int mode,
+                            cudaStream_t s) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const int Rpad = zrows ? t.KzPad : t.KpPad, Cpad = zrows ? t.KpPad : t.KzPad;
+  float* rterm2 = reinterpret_cast<float*>(w + t.rterm2);
+  float* sgn = reinterpret_cast<float*>(w + t.sgn);
+  int n = 0;
+  if (mode == 1) {
+    tc::RowtermArgs r{};
+    r.ell = a.ell; r.w = a.w;
+    r.beta = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
+    r.betaStride = t.KpPad; r.R = a.R; r.Rpad = Rpad;
+    r.rterm2 = rterm2; r.sgn = sgn;
+    tc::tc_rowterm_kernel<<<a.B, 256, 0, s>>>(r);
+    ++n;
+  }
+  tc::BwdArgs f{};
+  const bool own_rows = (mode == 1);
+  const uint8_t* rowT = zrows ? w + t.xt : w + t.yt;
+  const uint8_t* colT = zrows ? w + t.yt : w + t.xt;
+  f.Ot = own_rows ? rowT : colT;
+  f.Tt = own_rows ? colT : rowT;
+  f.o_tiles = (own_rows ? Rpad : Cpad) / 128;
+  f.t_tiles = (own_rows ? Cpad : Rpad) / 128;
+  f.ho = own_rows ? rterm2 : reinterpret_cast<const float*>(w + t.cb2);
+  f.ht = own_rows ? reinterpret_cast<const float*>(w + t.cb2) : rterm2;
+  f.sgn = sgn;
+  f.M = own_rows ? a.R : a.C;
+  f.B = a.B;
+  const bool owner_is_z = (own_rows == zrows);
+  f.owner_z = owner_is_z ? 1 : 0;
+  f.z = a.z; f.mu = a.mu; f.lv = a.lv;
+  f.shift = reinterpret_cast<const float*>(w + t.shift);
+  f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
+  f.rowsum = own_rows ? nullptr : a.colsum;
+  tc_bwd_launch<32>(f, s);
+  return n + 1;
 }
 
 inline bool tc_factors_ok(int, int, int) { return false; }
