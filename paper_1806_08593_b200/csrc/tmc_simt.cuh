@@ -466,5 +466,106 @@ __global__ void validate_kernel(const float* x, int64_t n, int allow_neginf, int
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Root edge of a DOWN chain (K_p = 1: the prior P(z_0)).  The pair matrix is K x 1, so
+// the "contraction" is elementwise in a: one warp per sample row, lanes over the D dimensions.
+//   fwd:  ell[a] = g[a] + cb[0] - cbmax,  out[a] = rb[a] + ell[a] - lnC      (g = log N(z_a; mu_0, e^{v_0}))
+//   row owner (MODE 1): P[a] = w[a] (softmax over one column), dz = P (mu - z) lam, pair = P
+//   column owner (MODE 2): colsum = sum_a P[a], dmu = sum_a P (z - mu) lam, dv = 1/2 sum_a P ((z-mu)^2 lam - 1)
+// Same arithmetic as pass_kernel<true, MODE, false, *> with C = 1.
+__global__ void __launch_bounds__(256) root_down_fwd_kernel(const PassArgs a) {
+  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D = a.D;
+  float cb0 = a.cb[b];
+  const float cbmax = (cb0 == -INFINITY) ? 0.f : cb0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.cbmax[b] = cbmax;
+    double off = (double)cbmax;
+    if (a.off_cb) off += a.off_cb[b];
+    if (a.off_rb) off += a.off_rb[b];
+    a.off_out[b] = off;
+  }
+  const float* mu = a.mu + (int64_t)b * D;
+  const float* lv = a.lv + (int64_t)b * D;
+  for (int r = blockIdx.x * 8 + warp; r < a.R; r += gridDim.x * 8) {
+    const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
+    float s = 0.f;
+    for (int d = lane; d < D; d += 32) {
+      const float df = z[d] - mu[d], v = lv[d];
+      s += df * df * __expf(-v) + v + kLog2Pi;
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const float e = (cb0 == -INFINITY) ? -INFINITY : -0.5f * s + (cb0 - cbmax);
+      a.ell[(int64_t)b * a.R + r] = e;
+      const float rb = a.rb ? a.rb[(int64_t)b * a.R + r] : 0.f;
+      a.out[(int64_t)b * a.R + r] = rb + e - a.lnC;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) root_down_row_kernel(const PassArgs a) {
+  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D = a.D;
+  const float* mu = a.mu + (int64_t)b * D;
+  const float* lv = a.lv + (int64_t)b * D;
+  for (int r = blockIdx.x * 8 + warp; r < a.R; r += gridDim.x * 8) {
+    const float e = a.ell[(int64_t)b * a.R + r];
+    const float P = (e == -INFINITY) ? 0.f : a.w[(int64_t)b * a.R + r];
+    if (a.pair && lane == 0) a.pair[(int64_t)b * a.R + r] = P;
+    if (a.gz) {
+      const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
+      float* gz = a.gz + ((int64_t)b * a.Kz + r) * D;
+      for (int d = lane; d < D; d += 32) gz[d] = P * (mu[d] - z[d]) * __expf(-lv[d]);
+    }
+  }
+}
+
+// one CTA per datapoint: reduce over the K rows
+__global__ void __launch_bounds__(256) root_down_col_kernel(const PassArgs a) {
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D = a.D;
+  __shared__ float red[3][8][33];
+  const float* mu = a.mu + (int64_t)b * D;
+  const float* lv = a.lv + (int64_t)b * D;
+  const float* w = a.w + (int64_t)b * a.R;
+  const float* ell = a.ell + (int64_t)b * a.R;
+  float psum = 0.f;
+  for (int d0 = 0; d0 < D; d0 += 32) {
+    const int d = d0 + lane;
+    float am = 0.f, av = 0.f;
+    const float m = d < D ? mu[d] : 0.f, lam = d < D ? __expf(-lv[d]) : 0.f;
+    for (int r = warp; r < a.R; r += 8) {
+      const float P = (ell[r] == -INFINITY) ? 0.f : w[r];
+      if (d0 == 0) psum += P;
+      if (d < D) {
+        const float df = a.z[((int64_t)b * a.Kz + r) * D + d] - m;
+        am += P * df * lam;
+        av += P * (df * df * lam - 1.f);
+      }
+    }
+    red[0][warp][lane] = am;
+    red[1][warp][lane] = av;
+    if (d0 == 0) red[2][warp][lane] = psum;
+    __syncthreads();
+    if (warp == 0) {
+      float sm = 0.f, sv = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { sm += red[0][k][lane]; sv += red[1][k][lane]; }
+      if (d < D) {
+        if (a.gmu) a.gmu[(int64_t)b * D + d] = sm;
+        if (a.glv) a.glv[(int64_t)b * D + d] = 0.5f * sv;
+      }
+      if (d0 == 0) {
+        float sp = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sp += red[2][k][lane];   // lanes hold per-warp partials
+        if (lane == 0 && a.colsum) a.colsum[b] = sp;           // every lane of a warp added the same P
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace simt
 }  // namespace tmc

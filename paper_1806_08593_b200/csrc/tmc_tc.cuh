@@ -332,8 +332,8 @@ template <int D>
 __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArgs a) {
   using G = Geo<D>;
   constexpr int RB = G::RB, ST = G::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared window
   uint8_t* sA = smem;                                   // RB tiles
   uint8_t* sB = sA + (size_t)RB * G::TILE;              // ST tiles
   float* sCb = reinterpret_cast<float*>(sB + (size_t)ST * G::TILE);   // ST x 128
@@ -462,14 +462,23 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[as]);
         mbar_wait(&cb_full[s], (t / ST) & 1);
-        const float* cbt = sCb + s * 128;
+        const float4* cbt = reinterpret_cast<const float4*>(sCb + s * 128);
         float* x = reinterpret_cast<float*>(v);
-        float tmax = -INFINITY;
+        float mx[8];
 #pragma unroll
-        for (int k = 0; k < 128; ++k) {
-          x[k] = __uint_as_float(v[k]) + cbt[k];
-          tmax = fmaxf(tmax, x[k]);
+        for (int q = 0; q < 32; ++q) {
+          const float4 c4 = cbt[q];
+          x[4 * q + 0] = __uint_as_float(v[4 * q + 0]) + c4.x;
+          x[4 * q + 1] = __uint_as_float(v[4 * q + 1]) + c4.y;
+          x[4 * q + 2] = __uint_as_float(v[4 * q + 2]) + c4.z;
+          x[4 * q + 3] = __uint_as_float(v[4 * q + 3]) + c4.w;
+          // 8 independent 3-input max chains (FMNMX3), tree-combined below
+          const int c = q & 7;
+          mx[c] = (q < 8) ? fmaxf(x[4 * q], fmaxf(x[4 * q + 1], fmaxf(x[4 * q + 2], x[4 * q + 3])))
+                          : fmaxf(mx[c], fmaxf(fmaxf(x[4 * q], x[4 * q + 1]), fmaxf(x[4 * q + 2], x[4 * q + 3])));
         }
+        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         __syncwarp();
         if (lane == 0) mbar_arrive(&cb_empty[s]);
         if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
@@ -510,18 +519,22 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
 // ------------------------------------------------------------------------------ K4: reverse pass
 // One "owner" pass of the reverse contraction.  The CTA owns 128 rows m of one
 // datapoint and streams the other side in 128-wide tiles n:
-//   P~[m,n] = ex2(S2[m,n] + ho[m] + ht[n] + 14)          (= 2^14 |w| exp(logf + bias - ell))
+//   P~[m,n] = ex2(S2[m,n] + ho[m] + ht[n] + 14)          (= 2^14 |w|/wscale exp(logf + bias - ell))
 //   G[m,:] += sum_n P~[m,n] T[n,:]                         (tcgen05, P~ and T both fp16 hi/lo)
 //   rowsum[m] = sum_n P~[m,n]
-// S is recomputed on tensor cores exactly as in the forward; P~ is written (swizzled, hi/lo) to
-// shared memory and is the A operand of the gradient GEMM, whose B operand is the streamed tile
-// itself read MN-major.  The epilogue turns G into dz (T = Y tiles) or dmu/dlogvar (T = X tiles).
+// S is recomputed on tensor cores exactly as in the forward.  P~ is split into fp16 hi/lo and
+// stored back into the TMEM columns its S tile came from (hi in the first 32 columns of each
+// 64-column half, lo in the second), where it is the A operand (tcgen05.mma A-from-TMEM) of the
+// gradient GEMM whose B operand is the streamed tile itself read MN-major; the S buffer is released
+// to the next S MMA by the commit of that gradient GEMM.  Eight softmax warps: two per TMEM lane
+// quarter, each owning one 64-column half of the tile.  The epilogue turns G into dz (T = Y tiles)
+// or dmu/dlogvar (T = X tiles).
 struct BwdArgs {
   const uint8_t *Ot, *Tt;      // owned / streamed tile images [B][tiles][TILE]
   int o_tiles, t_tiles;
   const float* ho;             // [B][o_tiles*128] owned log2 term
   const float* ht;             // [B][t_tiles*128] streamed log2 term (-inf padded)
-  const float* sgn;            // [B] sign of the upstream weights
+  const float* sgn;            // [B] signed scale of the upstream weights (w = sgn * |w|/|sgn|)
   int M, B;
   int owner_z;                 // 1: G = sum P Y -> dz ; 0: G = sum P X -> dmu, dlogvar
   const float *z, *mu, *lv;    // owner-side fp32 inputs [B][M][D]
@@ -535,11 +548,11 @@ struct BGeo {
   static constexpr int TILE = Geo<D>::TILE;
   static constexpr int PART = Geo<D>::PART;
   static constexpr int ATOMS = Geo<D>::ATOMS;
-  static constexpr int ST = 3;
-  static constexpr int THREADS = 192;
-  static constexpr int PBYTES = 2 * 2 * kAtomBytes;            // P~ hi + lo, 128 x 128 fp16 each
+  static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
+  static constexpr int SMW = 8;                                // softmax warps
+  static constexpr int THREADS = 64 + 32 * SMW;
   static constexpr int GCOL = 256;                             // TMEM column of the gradient accumulator
-  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + PBYTES + ST * 512 + 512;
+  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 2 * 128 * 4 + 512;
 };
 
 // MN-major SWIZZLE_128B descriptor: LBO = stride of 64-element MN chunks, SBO = 8-row K groups.
@@ -547,7 +560,36 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]  (A K-major in TMEM: lane = row, fp16 pairs per 32-bit column)
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+#define TMC_ST32(taddr, v)                                                                                          \
+  asm volatile(                                                                                                     \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"  \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                                 \
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),           \
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),    \
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),   \
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                                    \
+      : "memory")
+
+#define TMC_LD16(taddr, v)                                                                                          \
+  asm volatile(                                                                                                     \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"       \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),            \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])       \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int D>
 __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdArgs a) {
@@ -555,23 +597,22 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   constexpr int ST = G::ST;
   constexpr uint32_t IDESC_S = kIdescF16M128N128;
   constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | ((uint32_t)(2 * D) >> 3 << 17) | ((128u >> 4) << 24);
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sO = smem;
   uint8_t* sT = sO + G::TILE;
-  uint8_t* sP = sT + (size_t)ST * G::TILE;
-  float* sHt = reinterpret_cast<float*>(sP + G::PBYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sHt + ST * 128);
+  float* sHt = reinterpret_cast<float*>(sT + (size_t)ST * G::TILE);
+  float* sRs = sHt + ST * 128;                              // [2 (unit parity)][2 (half)][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRs + 512);
   uint64_t* o_full = bars + 0;
   uint64_t* o_empty = bars + 1;
   uint64_t* t_full = bars + 2;              // [ST]
   uint64_t* t_empty = bars + 2 + ST;        // [ST]
   uint64_t* h_full = bars + 2 + 2 * ST;     // [ST]
   uint64_t* h_empty = bars + 2 + 3 * ST;    // [ST]
-  uint64_t* s_full = bars + 2 + 4 * ST;     // [2]
-  uint64_t* s_empty = bars + 4 + 4 * ST;    // [2]
-  uint64_t* p_full = bars + 6 + 4 * ST;
-  uint64_t* p_empty = bars + 7 + 4 * ST;
+  uint64_t* s_full = bars + 2 + 4 * ST;     // [2]  S tile ready in TMEM buffer
+  uint64_t* s_empty = bars + 4 + 4 * ST;    // [2]  buffer free (its P~ consumed by the gradient GEMM)
+  uint64_t* p_full = bars + 6 + 4 * ST;     // [2]  P~ written back into the buffer
   uint64_t* g_full = bars + 8 + 4 * ST;
   uint64_t* g_empty = bars + 9 + 4 * ST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 4 * ST);
@@ -583,11 +624,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     mbar_init(o_empty, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
-      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], 4);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], G::SMW);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 4); }
-    mbar_init(p_full, 4); mbar_init(p_empty, 1);
-    mbar_init(g_full, 1); mbar_init(g_empty, 4);
+    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], G::SMW); }
+    mbar_init(g_full, 1); mbar_init(g_empty, G::SMW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -622,23 +662,24 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   } else if (warp == 1) {
     if (lane == 0) {   // ---------------- MMA issuer
       uint32_t t = 0, ua = 0;
-      const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT), pBase = smem_u32(sP);
+      const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
       auto grad = [&](uint32_t tt, bool first) {
-        mbar_wait(p_full, tt & 1);
+        const uint32_t as = tt & 1;
+        mbar_wait(&p_full[as], (tt >> 1) & 1);
         if (first) mbar_wait(g_empty, (ua & 1) ^ 1);
         tc_fence_after();
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
+        const uint32_t pA = tmem + as * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t po = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-          const uint64_t phi = sdesc(pBase + po), plo = sdesc(pBase + 2 * kAtomBytes + po);
+          const uint32_t phi = pA + (kk >> 2) * 64 + (kk & 3) * 8, plo = phi + 32;
           const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
-          mma_f16(tmem + G::GCOL, phi, thi, IDESC_G, (!first || kk) ? 1u : 0u);
-          mma_f16(tmem + G::GCOL, phi, tlo, IDESC_G, 1u);
-          mma_f16(tmem + G::GCOL, plo, thi, IDESC_G, 1u);
+          mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, (!first || kk) ? 1u : 0u);
+          mma_f16_ts(tmem + G::GCOL, phi, tlo, IDESC_G, 1u);
+          mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, 1u);
         }
         mma_commit(&t_empty[tt % ST]);
-        mma_commit(p_empty);
+        mma_commit(&s_empty[as]);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         mbar_wait(o_full, ua & 1);
@@ -674,9 +715,12 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       }
     }
   } else {
-    // ---------------- softmax / P~ producer warps (4) + epilogue
-    const int quarter = warp & 3;
+    // ---------------- softmax / P~ warps (8) + epilogue
+    const int sw = warp - 2;
+    const int quarter = warp & 3;               // TMEM lane quarter this warp may access
+    const int half = sw >> 2;                   // 64-column half of the tile (and half of the dims)
     const int m = quarter * 32 + lane;          // owned row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
       const int b = u / a.o_tiles, mt = u % a.o_tiles;
@@ -687,92 +731,114 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         const int as = t & 1, s = t % ST;
         mbar_wait(&s_full[as], (t >> 1) & 1);
         tc_fence_after();
-        uint32_t v[128];
-        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * 128);
+        uint32_t v[64];
+        const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + half * 64);
         TMC_LD32(taddr + 0, (v + 0));
         TMC_LD32(taddr + 32, (v + 32));
-        TMC_LD32(taddr + 64, (v + 64));
-        TMC_LD32(taddr + 96, (v + 96));
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[as]);
         mbar_wait(&h_full[s], (t / ST) & 1);
-        float* x = reinterpret_cast<float*>(v);
-        const float* hts = sHt + s * 128;
+        const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + half * 64);
+        uint32_t hi[32], lo[32];
         if (hom > -INFINITY) {
+          float r0 = 0.f, r1 = 0.f;
 #pragma unroll
-          for (int k = 0; k < 128; ++k) {
-            x[k] = ex2(__uint_as_float(v[k]) + hts[k] + hom);
-            rsum += x[k];
+          for (int q = 0; q < 16; ++q) {
+            const float4 h4 = hts[q];
+            const float p0 = ex2(__uint_as_float(v[4 * q + 0]) + h4.x + hom);
+            const float p1 = ex2(__uint_as_float(v[4 * q + 1]) + h4.y + hom);
+            const float p2 = ex2(__uint_as_float(v[4 * q + 2]) + h4.z + hom);
+            const float p3 = ex2(__uint_as_float(v[4 * q + 3]) + h4.w + hom);
+            r0 += p0 + p1;
+            r1 += p2 + p3;
+            __half2 h01 = __floats2half2_rn(p0, p1), h23 = __floats2half2_rn(p2, p3);
+            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+            __half2 l01 = __floats2half2_rn(p0 - f01.x, p1 - f01.y), l23 = __floats2half2_rn(p2 - f23.x, p3 - f23.y);
+            hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
+            hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
+            lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
+            lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
           }
+          rsum += r0 + r1;
         } else {
 #pragma unroll
-          for (int k = 0; k < 128; ++k) x[k] = 0.f;
+          for (int q = 0; q < 32; ++q) { hi[q] = 0u; lo[q] = 0u; }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
-        mbar_wait(p_empty, (t & 1) ^ 1);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float p0 = x[c * 8 + 2 * q], p1 = x[c * 8 + 2 * q + 1];
-            __half2 h = __floats2half2_rn(p0, p1);
-            float2 hf = __half22float2(h);
-            __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
-            hi[q] = *reinterpret_cast<uint32_t*>(&h);
-            lo[q] = *reinterpret_cast<uint32_t*>(&l);
-          }
-          const uint32_t off = swz_off(m, c * 8);
-          *reinterpret_cast<uint4*>(sP + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(sP + 2 * kAtomBytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        fence_proxy_async();
+        TMC_ST32(taddr, hi);
+        TMC_ST32(taddr + 32, lo);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (lane == 0) mbar_arrive(&p_full[as]);
       }
-      // ---------------- epilogue: G -> gradients
+      // ---------------- epilogue: G -> gradients (this warp: dims [half*D/2, (half+1)*D/2))
+      constexpr int DH = D / 2;
       mbar_wait(g_full, ua & 1);
       tc_fence_after();
-      float g[2 * D];
+      float g0[DH], g1[DH];          // G[:, d] and G[:, D + d] for this warp's dims
       {
-        uint32_t* gv = reinterpret_cast<uint32_t*>(g);
-        const uint32_t gaddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)G::GCOL;
-#pragma unroll
-        for (int c = 0; c < 2 * D / 32; ++c) TMC_LD32(gaddr + 32 * c, (gv + 32 * c));
+        uint32_t* r0 = reinterpret_cast<uint32_t*>(g0);
+        uint32_t* r1 = reinterpret_cast<uint32_t*>(g1);
+        const uint32_t gaddr = tmem + lane_off + (uint32_t)G::GCOL + half * DH;
+        if constexpr (DH == 16) {
+          TMC_LD16(gaddr, r0);
+          TMC_LD16(gaddr + D, r1);
+        } else {
+          TMC_LD32(gaddr, r0);
+          TMC_LD32(gaddr + D, r1);
+        }
         tmem_ld_wait();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(g_empty);
+      float* rs = sRs + (ua & 1) * 256;
+      rs[half * 128 + m] = rsum;
+      named_bar(1, 32 * G::SMW);
+      const float rtot = rs[m] + rs[128 + m];
       if (gm < a.M) {
         const float sc = a.sgn[b] * (1.f / 16384.f);
-        const float pi = rsum * sc;
-        const float* sh = a.shift + (size_t)b * D;
-        const size_t row = ((size_t)b * a.M + gm) * D;
+        const float pi = rtot * sc;
+        const float* sh = a.shift + (size_t)b * D + half * DH;
+        const size_t row = ((size_t)b * a.M + gm) * D + half * DH;
         if (a.owner_z) {
           // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
           if (a.gz) {
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-              const float zp = a.z[row + d] - sh[d];
-              a.gz[row + d] = (g[D + d] + 2.f * zp * g[d]) * (sc * kLn2);
+            for (int d4 = 0; d4 < DH; d4 += 4) {
+              const float4 z4 = *reinterpret_cast<const float4*>(a.z + row + d4);
+              const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+              float o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float zp = zz[e] - sh[d4 + e];
+                o[e] = (g1[d4 + e] + 2.f * zp * g0[d4 + e]) * (sc * kLn2);
+              }
+              *reinterpret_cast<float4*>(a.gz + row + d4) = make_float4(o[0], o[1], o[2], o[3]);
             }
           }
         } else {
           // G = sum P (X = [z'^2, z']): A2 = sum P z'^2, A1 = sum P z'
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const float mp = a.mu[row + d] - sh[d];
-            const float lam = __expf(-a.lv[row + d]);
-            const float A1 = g[D + d] * sc, A2 = g[d] * sc;
-            if (a.gmu) a.gmu[row + d] = lam * (A1 - mp * pi);
-            if (a.glv) a.glv[row + d] = 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+          for (int d4 = 0; d4 < DH; d4 += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(a.mu + row + d4);
+            const float4 v4 = *reinterpret_cast<const float4*>(a.lv + row + d4);
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+            float om[4], ov[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float mp = mm[e] - sh[d4 + e];
+              const float lam = __expf(-vv[e]);
+              const float A1 = g1[d4 + e] * sc, A2 = g0[d4 + e] * sc;
+              om[e] = lam * (A1 - mp * pi);
+              ov[e] = 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+            }
+            if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d4) = make_float4(om[0], om[1], om[2], om[3]);
+            if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
           }
         }
-        if (a.rowsum) a.rowsum[(size_t)b * a.M + gm] = pi;
+        if (a.rowsum && half == 0) a.rowsum[(size_t)b * a.M + gm] = pi;
       }
     }
   }
@@ -784,8 +850,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   }
 }
 
-// Per-row terms of the reverse pass: rterm2[r] = log2|w[r]| - (ell[r] - beta[r]) log2e (-inf when
-// the row carries no weight), sgn[b] = sign of the (uniformly signed) upstream weights.
+// Per-row terms of the reverse pass: rterm2[r] = log2(|w[r]|/ws) - (ell[r] - beta[r]) log2e (-inf when
+// the row carries no weight) and sgn[b] = +-ws, where ws = 2^ceil(log2 max_r |w[r]|) keeps the fp16
+// P~ <= 2^14 whatever the magnitude of dlogp, and the sign is that of the (uniformly signed, R2)
+// upstream weights.
 struct RowtermArgs {
   const float *ell, *w, *beta;   // [B][R], [B][R], [B][betaStride] (UP: beta of the row side) or NULL
   int betaStride, R, Rpad;
@@ -794,10 +862,22 @@ struct RowtermArgs {
 };
 
 __global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float red[8];
   __shared__ int neg;
   if (tid == 0) neg = 0;
+  float wm = 0.f;
+  for (int r = tid; r < a.R; r += 256) wm = fmaxf(wm, fabsf(a.w[(size_t)b * a.R + r]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+  if (lane == 0) red[warp] = wm;
   __syncthreads();
+  wm = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) wm = fmaxf(wm, red[w]);
+  // power-of-two scale (exact division); 1 when all weights are 0
+  const float lw = (wm > 0.f) ? ceilf(__log2f(wm)) : 0.f;
+  const float ws = exp2f(lw);
   for (int r = tid; r < a.Rpad; r += 256) {
     float v = -INFINITY;
     if (r < a.R) {
@@ -805,13 +885,13 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
       if (w < 0.f) neg = 1;
       if (e > -INFINITY && w != 0.f) {
         const float bt = a.beta ? a.beta[(size_t)b * a.betaStride + r] : 0.f;
-        v = __log2f(fabsf(w)) - (e - bt) * kLog2E;
+        v = __log2f(fabsf(w)) - lw - (e - bt) * kLog2E;
       }
     }
     a.rterm2[(size_t)b * a.Rpad + r] = v;
   }
   __syncthreads();
-  if (tid == 0) a.sgn[b] = neg ? -1.f : 1.f;
+  if (tid == 0) a.sgn[b] = neg ? -ws : ws;
 }
 
 }  // namespace tc
@@ -821,7 +901,7 @@ struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
   size_t xt = 0, yt = 0, beta = 0, cb2 = 0, shift = 0, rterm2 = 0, sgn = 0;
-  bool bwd_ok = false;      // reverse pass on tensor cores (D == 32)
+  bool bwd_ok = false;      // reverse pass on tensor cores
 };
 
 inline bool tc_dim_ok(int D) { return D == 32 || D == 64; }
@@ -864,7 +944,7 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     t.shift = tc_carve(cur, Bn * D[i] * 4);
     t.rterm2 = tc_carve(cur, Bn * Rpad * 4);
     t.sgn = tc_carve(cur, Bn * 4);
-    t.bwd_ok = (D[i] == 32);
+    t.bwd_ok = true;
   }
 }
 
@@ -1001,7 +1081,8 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
   f.shift = reinterpret_cast<const float*>(w + t.shift);
   f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
   f.rowsum = own_rows ? nullptr : a.colsum;
-  tc_bwd_launch<32>(f, s);
+  if (t.D == 32) tc_bwd_launch<32>(f, s);
+  else tc_bwd_launch<64>(f, s);
   return n + 1;
 }
 
