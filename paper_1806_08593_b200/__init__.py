@@ -13,7 +13,7 @@ import os
 from typing import Dict, List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtmc.so")
+LIB_PATH = os.environ.get("TMC_LIB_PATH") or os.path.join(_HERE, "libtmc.so")
 
 TMC_DIR_AUTO, TMC_DIR_DOWN, TMC_DIR_UP = 0, 1, 2
 TMC_PREC_AUTO, TMC_PREC_SIMT, TMC_PREC_TC = 0, 1, 2

@@ -17,6 +17,18 @@ def sources():
         + [os.path.join(ROOT, "include", "tmc.h")]
 
 
+def build_instrumented(verbose: bool = False) -> str:
+    """libtmc_instr.so: the same library with per-CTA barrier-wait counters (experiments only)."""
+    out = os.path.join(HERE, "libtmc_instr.so")
+    if os.path.exists(out) and all(os.path.getmtime(s) <= os.path.getmtime(out) for s in sources()):
+        return out
+    cmd = [NVCC] + FLAGS + ["-DTMC_INSTRUMENT", "-o", out, SRC]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT):
         t = os.path.getmtime(OUT)

@@ -19,6 +19,7 @@
 //                          with tcgen05.ld and run the online-max log2-sum-exp2 (ex2.approx, MUFU).
 #pragma once
 #include <cstddef>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 #include <cuda_fp16.h>
@@ -40,11 +41,12 @@ struct Geo {
   static constexpr int TILE = 2 * PART;              // hi + lo
   static constexpr int RB = (D <= 32) ? 2 : 1;       // 128-row blocks per CTA work unit
   static constexpr int STAGES = (D <= 32) ? 3 : 2;   // B-tile ring depth
-  static constexpr int SOFTMAX_WARPS = 4 * RB;
+  static constexpr int SOFTMAX_WARPS = 8 * RB;        // 2 per (TMEM lane quarter, row block): column halves
   static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS;
   static constexpr int TMEM_COLS = RB * 2 * 128;
   static constexpr size_t SMEM = 1024 /*align*/ + (size_t)RB * TILE + (size_t)STAGES * TILE +
-                                 (size_t)STAGES * 128 * 4 + 512 /*barriers*/;
+                                 (size_t)STAGES * 128 * 4 + (size_t)RB * 128 * 8 /*half merge*/ +
+                                 512 /*barriers*/;
 };
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -73,6 +75,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Optional instrumentation (-DTMC_INSTRUMENT builds libtmc_instr.so only): cycles each role spends
+// waiting on each barrier, per CTA, read back with tmc_debug_counters().
+#ifdef TMC_INSTRUMENT
+__device__ unsigned long long g_tmc_prof[1024][16];
+#define TMC_PROF_WAIT(cond, slot, call)                                                   \
+  do {                                                                                    \
+    const long long _t0 = clock64();                                                      \
+    call;                                                                                 \
+    if (cond) atomicAdd(&g_tmc_prof[blockIdx.x & 1023][slot], (unsigned long long)(clock64() - _t0)); \
+  } while (0)
+#define TMC_PROF_T0(var) const long long var = clock64()
+#define TMC_PROF_END(cond, slot, var) \
+  if (cond) atomicAdd(&g_tmc_prof[blockIdx.x & 1023][slot], (unsigned long long)(clock64() - var))
+#else
+#define TMC_PROF_WAIT(cond, slot, call) call
+#define TMC_PROF_T0(var)
+#define TMC_PROF_END(cond, slot, var)
+#endif
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -114,6 +134,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])     \
       : "r"(taddr))
 
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -212,59 +233,84 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
     }
     __syncthreads();
   }
-  constexpr int PER = D / 32;     // dims per lane
+  // Tile images: one thread per (row, 8-feature chunk) writes 16 B of the hi part and 16 B of the lo
+  // part (8 consecutive chunk-threads fill one 128-byte swizzled row of an atom: coalesced).
+  constexpr int CPR = D / 4;           // 8-feature chunks per row (2D features)
+  constexpr int HC = D / 8;            // chunks of the first half ([z'^2] / [-lam/2])
+  constexpr int RPI = 256 / CPR;       // rows per iteration of the CTA
+  const int j = tid % CPR, rsub = tid / CPR;
+  const int dj = (j < HC ? j : j - HC) * 8;
   uint8_t* Yb = p.Yt + (size_t)b * (p.KpPad / kTileRows) * G::TILE;
   uint8_t* Xb = p.Xt + (size_t)b * (p.KzPad / kTileRows) * G::TILE;
-  // param rows -> Y tile image, beta
-  for (int c = warp; c < p.KpPad; c += 8) {
-    float bsum = 0.f;
-    uint8_t* tile = Yb + (size_t)(c / kTileRows) * G::TILE;
-    const int r = c % kTileRows;
+  float sh[8];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int d = lane + 32 * q;
-      float y0 = 0.f, y1 = 0.f;
-      if (c < p.Kp) {
-        float v = lvb[(size_t)c * D + d];
-        float lam = __expf(-v);
-        float mp = mub[(size_t)c * D + d] - s_shift[d];
-        y0 = -0.5f * lam * kLog2E;
-        y1 = lam * mp * kLog2E;
-        bsum += lam * mp * mp + v + kLog2Pi;
-      }
-      __half h, l;
-      split16(y0, h, l);
-      *reinterpret_cast<__half*>(tile + swz_off(r, d)) = h;
-      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, d)) = l;
-      split16(y1, h, l);
-      *reinterpret_cast<__half*>(tile + swz_off(r, D + d)) = h;
-      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, D + d)) = l;
+  for (int e = 0; e < 8; ++e) sh[e] = s_shift[dj + e];
+  auto store = [&](uint8_t* img, int row, const float* vals) {
+    uint8_t* tile = img + (size_t)(row / kTileRows) * G::TILE;
+    const int r = row % kTileRows;
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __half2 h = __floats2half2_rn(vals[2 * q], vals[2 * q + 1]);
+      const float2 hf = __half22float2(h);
+      __half2 l = __floats2half2_rn(vals[2 * q] - hf.x, vals[2 * q + 1] - hf.y);
+      hi[q] = *reinterpret_cast<uint32_t*>(&h);
+      lo[q] = *reinterpret_cast<uint32_t*>(&l);
     }
+    const uint32_t off = swz_off(r, j * 8);
+    *reinterpret_cast<uint4*>(tile + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(tile + G::PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  };
+  // param rows -> Y tile image, beta
+  for (int c0 = 0; c0 < p.KpPad; c0 += RPI) {
+    const int c = c0 + rsub;
+    float y[8];
+    float bsum = 0.f;
+    if (c < p.Kp) {
+      const float4* lv4 = reinterpret_cast<const float4*>(lvb + (size_t)c * D + dj);
+      const float4* mu4 = reinterpret_cast<const float4*>(mub + (size_t)c * D + dj);
+      const float4 va = lv4[0], vb = lv4[1], ma = mu4[0], mb = mu4[1];
+      const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+      const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
 #pragma unroll
-    for (int o = 16; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
-    if (lane == 0) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * bsum : 0.f;
+      for (int e = 0; e < 8; ++e) {
+        const float lam = __expf(-vv[e]);
+        const float mp = mm[e] - sh[e];
+        if (j < HC) {
+          y[e] = -0.5f * lam * kLog2E;
+          bsum += lam * mp * mp + vv[e] + kLog2Pi;
+        } else {
+          y[e] = lam * mp * kLog2E;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[e] = 0.f;
+    }
+    if (c < p.KpPad) store(Yb, c, y);
+    // beta: sum over the HC first-half chunk-threads of the row (lane groups of CPR)
+#pragma unroll
+    for (int o = CPR / 2; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    if (j == 0 && c < p.KpPad) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * bsum : 0.f;
   }
   // z rows -> X tile image
-  for (int a = warp; a < p.KzPad; a += 8) {
-    uint8_t* tile = Xb + (size_t)(a / kTileRows) * G::TILE;
-    const int r = a % kTileRows;
+  for (int a0 = 0; a0 < p.KzPad; a0 += RPI) {
+    const int a = a0 + rsub;
+    float x[8];
+    if (a < p.Kz) {
+      const float4* z4 = reinterpret_cast<const float4*>(zb + (size_t)a * D + dj);
+      const float4 za = z4[0], zc = z4[1];
+      const float zz[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int d = lane + 32 * q;
-      float x0 = 0.f, x1 = 0.f;
-      if (a < p.Kz) {
-        float zp = zb[(size_t)a * D + d] - s_shift[d];
-        x0 = zp * zp;
-        x1 = zp;
+      for (int e = 0; e < 8; ++e) {
+        const float zp = zz[e] - sh[e];
+        x[e] = (j < HC) ? zp * zp : zp;
       }
-      __half h, l;
-      split16(x0, h, l);
-      *reinterpret_cast<__half*>(tile + swz_off(r, d)) = h;
-      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, d)) = l;
-      split16(x1, h, l);
-      *reinterpret_cast<__half*>(tile + swz_off(r, D + d)) = h;
-      *reinterpret_cast<__half*>(tile + G::PART + swz_off(r, D + d)) = l;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = 0.f;
     }
+    if (a < p.KzPad) store(Xb, a, x);
   }
 }
 
@@ -326,6 +372,7 @@ struct FwdArgs {
   int R, B;
   float lnC;
   float *out, *ell;            // [B][R]
+  int dbg;                     // experiment flags (TMC_DEBUG_FLAGS; 0 in production): 1 no MMA, 2 no softmax math
 };
 
 template <int D>
@@ -337,7 +384,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   uint8_t* sA = smem;                                   // RB tiles
   uint8_t* sB = sA + (size_t)RB * G::TILE;              // ST tiles
   float* sCb = reinterpret_cast<float*>(sB + (size_t)ST * G::TILE);   // ST x 128
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sCb + ST * 128);
+  float2* sMerge = reinterpret_cast<float2*>(sCb + ST * 128);          // RB x 128 (max, sum) of half 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + RB * 128);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 1;
   uint64_t* b_full = bars + 2;            // [ST]
@@ -375,40 +423,44 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    TMC_PROF_T0(_tr0);
     // ===================== producer: bulk copies (TMA engine) =====================
     if (lane == 0) {
       uint32_t t = 0, ua = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         const int b = u / groups, g = u % groups;
-        mbar_wait(a_empty, (ua & 1) ^ 1);
+        TMC_PROF_WAIT(true, 2, mbar_wait(a_empty, (ua & 1) ^ 1));
         mbar_expect_tx(a_full, RB * G::TILE);
         bulk_g2s(sA, a.At + ((size_t)b * a.a_tiles + (size_t)g * RB) * G::TILE, RB * G::TILE, a_full);
         for (int j = 0; j < a.b_tiles; ++j, ++t) {
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
-          mbar_wait(&b_empty[s], ph);
+          TMC_PROF_WAIT(true, 0, mbar_wait(&b_empty[s], ph));
           mbar_expect_tx(&b_full[s], G::TILE);
           bulk_g2s(sB + (size_t)s * G::TILE, a.Bt + ((size_t)b * a.b_tiles + j) * G::TILE, G::TILE, &b_full[s]);
-          mbar_wait(&cb_empty[s], ph);
+          TMC_PROF_WAIT(true, 1, mbar_wait(&cb_empty[s], ph));
           mbar_expect_tx(&cb_full[s], 512);
           bulk_g2s(sCb + s * 128, a.cb2 + ((size_t)b * a.b_tiles + j) * 128, 512, &cb_full[s]);
         }
       }
     }
+    TMC_PROF_END(lane == 0, 14, _tr0);
   } else if (warp == 1) {
+    TMC_PROF_T0(_tr1);
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       uint32_t t = 0, ua = 0;
       const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        mbar_wait(a_full, ua & 1);
+        TMC_PROF_WAIT(true, 6, mbar_wait(a_full, ua & 1));
         for (int j = 0; j < a.b_tiles; ++j, ++t) {
           const int s = t % ST, as = t & 1;
-          mbar_wait(&b_full[s], (t / ST) & 1);
-          mbar_wait(&acc_empty[as], ((t >> 1) & 1) ^ 1);
+          TMC_PROF_WAIT(true, 3, mbar_wait(&b_full[s], (t / ST) & 1));
+          TMC_PROF_WAIT(true, 4, mbar_wait(&acc_empty[as], ((t >> 1) & 1) ^ 1));
           tc_fence_after();
 #pragma unroll
           for (int rb = 0; rb < RB; ++rb) {
+            if (a.dbg & 1) break;
             const uint32_t d = tmem + (uint32_t)((rb * 2 + as) * 128);
             const uint32_t A = aBase + rb * G::TILE, Bs = bBase + s * G::TILE;
             // small cross terms first, the large hi*hi products last: fewer fp32 accumulator
@@ -437,10 +489,15 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
         mma_commit(a_empty);
       }
     }
+    TMC_PROF_END(lane == 0, 12, _tr1);
   } else {
+    TMC_PROF_T0(_tr2);
     // ===================== softmax warps: TMEM -> online log2-sum-exp2 =====================
+    // warp -> (TMEM lane quarter, row block rb, column half): each thread owns one row of one
+    // 64-column half of every S tile; the two halves' (max, sum) states merge at the unit's end.
     const int sw = warp - 2;
-    const int rb = sw >> 2;
+    const int rb = (sw >> 2) % RB;
+    const int half = sw / (4 * RB);
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
     const int rloc = rb * 128 + quarter * 32 + lane;
     uint32_t t = 0;
@@ -449,36 +506,34 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
       float mref = -INFINITY, sum = 0.f;
       for (int j = 0; j < a.b_tiles; ++j, ++t) {
         const int as = t & 1, s = t % ST;
-        mbar_wait(&acc_full[as], (t >> 1) & 1);
+        TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&acc_full[as], (t >> 1) & 1));
         tc_fence_after();
-        uint32_t v[128];
-        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((rb * 2 + as) * 128);
+        uint32_t v[64];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((rb * 2 + as) * 128 + half * 64);
         TMC_LD32(taddr + 0, (v + 0));
         TMC_LD32(taddr + 32, (v + 32));
-        TMC_LD32(taddr + 64, (v + 64));
-        TMC_LD32(taddr + 96, (v + 96));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[as]);
-        mbar_wait(&cb_full[s], (t / ST) & 1);
-        const float4* cbt = reinterpret_cast<const float4*>(sCb + s * 128);
+        TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&cb_full[s], (t / ST) & 1));
+        if (a.dbg & 2) { __syncwarp(); if (lane == 0) mbar_arrive(&cb_empty[s]); sum += __uint_as_float(v[0]) + __uint_as_float(v[63]); continue; }
+        const float4* cbt = reinterpret_cast<const float4*>(sCb + s * 128 + half * 64);
         float* x = reinterpret_cast<float*>(v);
-        float mx[8];
+        float mx[4];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const float4 c4 = cbt[q];
           x[4 * q + 0] = __uint_as_float(v[4 * q + 0]) + c4.x;
           x[4 * q + 1] = __uint_as_float(v[4 * q + 1]) + c4.y;
           x[4 * q + 2] = __uint_as_float(v[4 * q + 2]) + c4.z;
           x[4 * q + 3] = __uint_as_float(v[4 * q + 3]) + c4.w;
-          // 8 independent 3-input max chains (FMNMX3), tree-combined below
-          const int c = q & 7;
-          mx[c] = (q < 8) ? fmaxf(x[4 * q], fmaxf(x[4 * q + 1], fmaxf(x[4 * q + 2], x[4 * q + 3])))
+          // 4 independent 3-input max chains (FMNMX3), tree-combined below
+          const int c = q & 3;
+          mx[c] = (q < 4) ? fmaxf(x[4 * q], fmaxf(x[4 * q + 1], fmaxf(x[4 * q + 2], x[4 * q + 3])))
                           : fmaxf(mx[c], fmaxf(fmaxf(x[4 * q], x[4 * q + 1]), fmaxf(x[4 * q + 2], x[4 * q + 3])));
         }
-        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         __syncwarp();
         if (lane == 0) mbar_arrive(&cb_empty[s]);
         if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
@@ -488,7 +543,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
         if (mref > -INFINITY) {
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-          for (int k = 0; k < 128; k += 4) {
+          for (int k = 0; k < 64; k += 4) {
             s0 += ex2(x[k] - mref);
             s1 += ex2(x[k + 1] - mref);
             s2 += ex2(x[k + 2] - mref);
@@ -497,15 +552,26 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
           sum += (s0 + s1) + (s2 + s3);
         }
       }
-      const int r = g * RB * 128 + rloc;
-      if (r < a.R) {
-        float e = (sum > 0.f) ? kLn2 * (mref + __log2f(sum)) : -INFINITY;
-        if (a.ell_add) e += a.ell_add[(size_t)b * a.ell_stride + r];
-        a.ell[(size_t)b * a.R + r] = e;
-        const float oa = a.out_add ? a.out_add[(size_t)b * a.R + r] : 0.f;
-        a.out[(size_t)b * a.R + r] = oa + e - a.lnC;
+      // merge the two column halves of each row (half 1 -> SMEM -> half 0)
+      if (half == 1) sMerge[rloc] = make_float2(mref, sum);
+      named_bar(1, 32 * G::SOFTMAX_WARPS);
+      if (half == 0) {
+        const float2 o = sMerge[rloc];
+        const float M = fmaxf(mref, o.x);
+        float tot = 0.f;
+        if (M > -INFINITY) tot = (mref > -INFINITY ? sum * ex2(mref - M) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - M) : 0.f);
+        const int r = g * RB * 128 + rloc;
+        if (r < a.R) {
+          float e = (tot > 0.f) ? kLn2 * (M + __log2f(tot)) : -INFINITY;
+          if (a.ell_add) e += a.ell_add[(size_t)b * a.ell_stride + r];
+          a.ell[(size_t)b * a.R + r] = e;
+          const float oa = a.out_add ? a.out_add[(size_t)b * a.R + r] : 0.f;
+          a.out[(size_t)b * a.R + r] = oa + e - a.lnC;
+        }
       }
+      named_bar(1, 32 * G::SOFTMAX_WARPS);   // sMerge is reused by the next unit
     }
+    TMC_PROF_END(warp == 2 && lane == 0, 13, _tr2);
   }
   tc_fence_before();
   __syncthreads();
@@ -541,6 +607,7 @@ struct BwdArgs {
   const float* shift;          // [B][D]
   float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
   float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
+  int dbg;                     // experiment flags: 1 no S MMA, 2 no gradient MMA, 4 no softmax math
 };
 
 template <int D>
@@ -589,14 +656,21 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       : "r"(taddr))
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int D>
+// GT = fp16 terms of the gradient GEMM:
+//   1 = P_hi T_hi, 2 = P_hi (T_lo + T_hi), 3 = P_lo T_hi + P_hi T_lo + P_hi T_hi  (N = 2D MMAs), and the
+//   packed forms, where one MMA of N = 4D reads the streamed tile's hi and lo parts side by side
+//   ([T_hi | T_lo] is exactly the tile image seen MN-major with LBO = one atom) and the epilogue adds
+//   the two column halves:  4 = P_hi [T_hi | T_lo],  5 = (P_hi + P_lo) [T_hi | T_lo].
+template <int D, int GT>
 __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdArgs a) {
   using G = BGeo<D>;
   constexpr int ST = G::ST;
   constexpr uint32_t IDESC_S = kIdescF16M128N128;
-  constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | ((uint32_t)(2 * D) >> 3 << 17) | ((128u >> 4) << 24);
+  constexpr bool PACKED = GT >= 4;
+  constexpr uint32_t GN = PACKED ? 4 * D : 2 * D;            // N of the gradient MMA
+  constexpr bool PLO = (GT == 3 || GT == 5);                 // P~ lo part needed
+  constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | (GN >> 3 << 17) | ((128u >> 4) << 24);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sO = smem;
@@ -640,57 +714,67 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    TMC_PROF_T0(_tr0);
     if (lane == 0) {   // ---------------- producer
       uint32_t t = 0, ua = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         const int b = u / a.o_tiles, mt = u % a.o_tiles;
-        mbar_wait(o_empty, (ua & 1) ^ 1);
+        TMC_PROF_WAIT(true, 2, mbar_wait(o_empty, (ua & 1) ^ 1));
         mbar_expect_tx(o_full, G::TILE);
         bulk_g2s(sO, a.Ot + ((size_t)b * a.o_tiles + mt) * G::TILE, G::TILE, o_full);
         for (int j = 0; j < a.t_tiles; ++j, ++t) {
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
-          mbar_wait(&t_empty[s], ph);
+          TMC_PROF_WAIT(true, 0, mbar_wait(&t_empty[s], ph));
           mbar_expect_tx(&t_full[s], G::TILE);
           bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, G::TILE, &t_full[s]);
-          mbar_wait(&h_empty[s], ph);
+          TMC_PROF_WAIT(true, 1, mbar_wait(&h_empty[s], ph));
           mbar_expect_tx(&h_full[s], 512);
           bulk_g2s(sHt + s * 128, a.ht + ((size_t)b * a.t_tiles + j) * 128, 512, &h_full[s]);
         }
       }
     }
+    TMC_PROF_END(lane == 0, 14, _tr0);
   } else if (warp == 1) {
+    TMC_PROF_T0(_tr1);
     if (lane == 0) {   // ---------------- MMA issuer
       uint32_t t = 0, ua = 0;
       const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
       auto grad = [&](uint32_t tt, bool first) {
         const uint32_t as = tt & 1;
-        mbar_wait(&p_full[as], (tt >> 1) & 1);
-        if (first) mbar_wait(g_empty, (ua & 1) ^ 1);
+        TMC_PROF_WAIT(true, 5, mbar_wait(&p_full[as], (tt >> 1) & 1));
+        if (first) TMC_PROF_WAIT(true, 7, mbar_wait(g_empty, (ua & 1) ^ 1));
         tc_fence_after();
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
         const uint32_t pA = tmem + as * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
+          if (a.dbg & 2) break;
           const uint32_t phi = pA + (kk >> 2) * 64 + (kk & 3) * 8, plo = phi + 32;
           const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
-          mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, (!first || kk) ? 1u : 0u);
-          mma_f16_ts(tmem + G::GCOL, phi, tlo, IDESC_G, 1u);
-          mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, 1u);
+          const uint32_t acc0 = (!first || kk) ? 1u : 0u;
+          if constexpr (PACKED) {
+            if constexpr (GT == 5) mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, acc0);
+            mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, GT == 5 ? 1u : acc0);
+          } else {
+            if constexpr (GT >= 3) mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, acc0);
+            if constexpr (GT >= 2) mma_f16_ts(tmem + G::GCOL, phi, tlo, IDESC_G, GT >= 3 ? 1u : acc0);
+            mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
+          }
         }
         mma_commit(&t_empty[tt % ST]);
         mma_commit(&s_empty[as]);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        mbar_wait(o_full, ua & 1);
+        TMC_PROF_WAIT(true, 6, mbar_wait(o_full, ua & 1));
         for (int j = 0; j < a.t_tiles; ++j, ++t) {
           const int s = t % ST, as = t & 1;
-          mbar_wait(&t_full[s], (t / ST) & 1);
-          mbar_wait(&s_empty[as], ((t >> 1) & 1) ^ 1);
+          TMC_PROF_WAIT(true, 3, mbar_wait(&t_full[s], (t / ST) & 1));
+          TMC_PROF_WAIT(true, 4, mbar_wait(&s_empty[as], ((t >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
 #pragma unroll
-          for (int at = 0; at < G::ATOMS; ++at) {
+          for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
@@ -699,7 +783,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
             }
           }
 #pragma unroll
-          for (int at = 0; at < G::ATOMS; ++at) {
+          for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
@@ -714,7 +798,9 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         mma_commit(o_empty);
       }
     }
+    TMC_PROF_END(lane == 0, 12, _tr1);
   } else {
+    TMC_PROF_T0(_tr2);
     // ---------------- softmax / P~ warps (8) + epilogue
     const int sw = warp - 2;
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
@@ -729,17 +815,17 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       float rsum = 0.f;
       for (int j = 0; j < a.t_tiles; ++j, ++t) {
         const int as = t & 1, s = t % ST;
-        mbar_wait(&s_full[as], (t >> 1) & 1);
+        TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t >> 1) & 1));
         tc_fence_after();
         uint32_t v[64];
         const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + half * 64);
         TMC_LD32(taddr + 0, (v + 0));
         TMC_LD32(taddr + 32, (v + 32));
         tmem_ld_wait();
-        mbar_wait(&h_full[s], (t / ST) & 1);
+        TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
         const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + half * 64);
         uint32_t hi[32], lo[32];
-        if (hom > -INFINITY) {
+        if (hom > -INFINITY && !(a.dbg & 4)) {
           float r0 = 0.f, r1 = 0.f;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
@@ -751,12 +837,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
             r0 += p0 + p1;
             r1 += p2 + p3;
             __half2 h01 = __floats2half2_rn(p0, p1), h23 = __floats2half2_rn(p2, p3);
-            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-            __half2 l01 = __floats2half2_rn(p0 - f01.x, p1 - f01.y), l23 = __floats2half2_rn(p2 - f23.x, p3 - f23.y);
             hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
             hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
-            lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
-            lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
+            if constexpr (PLO) {
+              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+              __half2 l01 = __floats2half2_rn(p0 - f01.x, p1 - f01.y), l23 = __floats2half2_rn(p2 - f23.x, p3 - f23.y);
+              lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
+              lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
+            }
           }
           rsum += r0 + r1;
         } else {
@@ -766,7 +854,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
         TMC_ST32(taddr, hi);
-        TMC_ST32(taddr + 32, lo);
+        if constexpr (PLO) TMC_ST32(taddr + 32, lo);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -774,7 +862,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       }
       // ---------------- epilogue: G -> gradients (this warp: dims [half*D/2, (half+1)*D/2))
       constexpr int DH = D / 2;
-      mbar_wait(g_full, ua & 1);
+      TMC_PROF_WAIT(sw == 0 && lane == 0, 10, mbar_wait(g_full, ua & 1));
       tc_fence_after();
       float g0[DH], g1[DH];          // G[:, d] and G[:, D + d] for this warp's dims
       {
@@ -787,6 +875,22 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         } else {
           TMC_LD32(gaddr, r0);
           TMC_LD32(gaddr + D, r1);
+        }
+        if constexpr (PACKED) {     // + the T_lo column half
+          uint32_t q0[DH], q1[DH];
+          if constexpr (DH == 16) {
+            TMC_LD16(gaddr + 2 * D, q0);
+            TMC_LD16(gaddr + 3 * D, q1);
+          } else {
+            TMC_LD32(gaddr + 2 * D, q0);
+            TMC_LD32(gaddr + 3 * D, q1);
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < DH; ++e) {
+            g0[e] += __uint_as_float(q0[e]);
+            g1[e] += __uint_as_float(q1[e]);
+          }
         }
         tmem_ld_wait();
       }
@@ -841,6 +945,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         if (a.rowsum && half == 0) a.rowsum[(size_t)b * a.M + gm] = pi;
       }
     }
+    TMC_PROF_END(warp == 2 && lane == 0, 13, _tr2);
   }
   tc_fence_before();
   __syncthreads();
@@ -897,6 +1002,14 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
 }  // namespace tc
 
 // ================================================================================ host side
+inline int tc_debug_flags() {   // read per launch (experiments flip it within one process)
+  const char* e = std::getenv("TMC_DEBUG_FLAGS");
+  return e ? std::atoi(e) : 0;
+}
+
+// Default number of fp16 terms of the reverse pass's gradient GEMM (TMC_BWD_GRAD_TERMS overrides).
+constexpr int kDefaultGradTerms = 3;
+
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
@@ -1018,17 +1131,24 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   f.out_add = a.rb;
   f.R = a.R; f.B = a.B; f.lnC = a.lnC;
   f.out = a.out; f.ell = a.ell;
+  f.dbg = tc_debug_flags() & 3;
   if (t.D == 32) tc_fwd_launch<32>(f, s);
   else tc_fwd_launch<64>(f, s);
   return 2;
 }
 
-template <int D>
-inline void tc_bwd_launch(const tc::BwdArgs& f, cudaStream_t s) {
+inline int tc_grad_terms() {
+  const char* e = std::getenv("TMC_BWD_GRAD_TERMS");
+  const int v = e ? std::atoi(e) : kDefaultGradTerms;
+  return (v >= 1 && v <= 5) ? v : kDefaultGradTerms;
+}
+
+template <int D, int GT>
+inline void tc_bwd_launch_t(const tc::BwdArgs& f, cudaStream_t s) {
   using G = tc::BGeo<D>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc::tc_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaFuncSetAttribute(tc::tc_bwd_kernel<D, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     attr = true;
   }
   static int sms = 0;
@@ -1039,7 +1159,18 @@ inline void tc_bwd_launch(const tc::BwdArgs& f, cudaStream_t s) {
   }
   const int units = f.B * f.o_tiles;
   const int grid = units < sms ? units : sms;
-  tc::tc_bwd_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
+  tc::tc_bwd_kernel<D, GT><<<grid, G::THREADS, G::SMEM, s>>>(f);
+}
+
+template <int D>
+inline void tc_bwd_launch(const tc::BwdArgs& f, cudaStream_t s) {
+  switch (tc_grad_terms()) {
+    case 1: return tc_bwd_launch_t<D, 1>(f, s);
+    case 2: return tc_bwd_launch_t<D, 2>(f, s);
+    case 4: return tc_bwd_launch_t<D, 4>(f, s);
+    case 5: return tc_bwd_launch_t<D, 5>(f, s);
+    default: return tc_bwd_launch_t<D, 3>(f, s);
+  }
 }
 
 inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.ok && t.bwd_ok && !a.pair; }
@@ -1081,6 +1212,7 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
   f.shift = reinterpret_cast<const float*>(w + t.shift);
   f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
   f.rowsum = own_rows ? nullptr : a.colsum;
+  f.dbg = (tc_debug_flags() >> 2) & 7;
   if (t.D == 32) tc_bwd_launch<32>(f, s);
   else tc_bwd_launch<64>(f, s);
   return n + 1;

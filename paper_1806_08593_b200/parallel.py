@@ -1,0 +1,48 @@
+"""Data-parallel plumbing of the TMC hot path.
+
+Datapoints are independent problems (each carries its own K proposal samples per latent),
+so rank r of W owns a contiguous slice of the global batch and every per-datapoint output stays
+local.  The one exchange is a SUM all-reduce of the objective J = sum_b logp[b] (and, in a training
+step, of shared-parameter gradients), issued on the caller's process group: NCCL over NVLink on
+the GPU box, gloo in the CPU tests.  No kernel code lives here.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+
+def shard_ids(B: int, rank: int, world: int) -> List[int]:
+    """Global datapoint ids owned by `rank` (contiguous, equal sizes; B must divide evenly)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    if B % world:
+        raise ValueError(f"B={B} is not divisible by world={world}")
+    per = B // world
+    return list(range(rank * per, (rank + 1) * per))
+
+
+def reduce_objective(local_sum, group=None):
+    """In-place SUM all-reduce of a float64 tensor holding this rank's partial objective(s)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(local_sum, op=dist.ReduceOp.SUM, group=group)
+    return local_sum
+
+
+def gather_per_datapoint(local, group=None):
+    """All-gather equal-sized per-datapoint tensors into global batch order (rank-major)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local
+    parts = [torch.empty_like(local) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, local.contiguous(), group=group)
+    return torch.cat(parts, dim=0)
+
+
+def max_over_ranks(values, group=None):
+    """In-place MAX all-reduce (device timings: the job time is the slowest rank's)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(values, op=dist.ReduceOp.MAX, group=group)
+    return values
