@@ -110,18 +110,25 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 // Instruction descriptor: kind::f16, A/B fp16 K-major, D fp32, M=128, N=128.
 constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
+// The MMA warp runs converged (descriptors stay in uniform registers); one elected lane issues.
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 #define TMC_LD32(taddr, v)                                                                                          \
@@ -141,6 +148,21 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (Cody-Waite range reduction + degree-5 minimax polynomial on [-1/2, 1/2],
+// max relative error 8e-8, below ex2.approx's 2^-22): used to move a fixed share of the forward's
+// exponentials off the MUFU pipe.  Valid for x <= 127 (callers guarantee x <= 8); x < -125 -> ~0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;            // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);       // f in [-1/2, 1/2]
+  float p = fmaf(1.3277400e-3f, f, 9.6758800e-3f);
+  p = fmaf(p, f, 5.5507130e-2f);
+  p = fmaf(p, f, 2.4022112e-1f);
+  p = fmaf(p, f, 6.9314696e-1f);
+  p = fmaf(p, f, 1.0000001f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 // Byte offset of element k (fp16 index within the part's row vector) of row r in a tile part
@@ -375,7 +397,7 @@ struct FwdArgs {
   int dbg;                     // experiment flags (TMC_DEBUG_FLAGS; 0 in production): 1 no MMA, 2 no softmax math
 };
 
-template <int D>
+template <int D, int NPOLY, bool MAXFREE>
 __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArgs a) {
   using G = Geo<D>;
   constexpr int RB = G::RB, ST = G::STAGES;
@@ -447,16 +469,16 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     TMC_PROF_END(lane == 0, 14, _tr0);
   } else if (warp == 1) {
     TMC_PROF_T0(_tr1);
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (whole warp, one elected lane issues) =====================
+    {
       uint32_t t = 0, ua = 0;
       const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        TMC_PROF_WAIT(true, 6, mbar_wait(a_full, ua & 1));
+        TMC_PROF_WAIT(lane == 0, 6, mbar_wait(a_full, ua & 1));
         for (int j = 0; j < a.b_tiles; ++j, ++t) {
           const int s = t % ST, as = t & 1;
-          TMC_PROF_WAIT(true, 3, mbar_wait(&b_full[s], (t / ST) & 1));
-          TMC_PROF_WAIT(true, 4, mbar_wait(&acc_empty[as], ((t >> 1) & 1) ^ 1));
+          TMC_PROF_WAIT(lane == 0, 3, mbar_wait(&b_full[s], (t / ST) & 1));
+          TMC_PROF_WAIT(lane == 0, 4, mbar_wait(&acc_empty[as], ((t >> 1) & 1) ^ 1));
           tc_fence_after();
 #pragma unroll
           for (int rb = 0; rb < RB; ++rb) {
@@ -518,38 +540,68 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
         if (lane == 0) mbar_arrive(&acc_empty[as]);
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&cb_full[s], (t / ST) & 1));
         if (a.dbg & 2) { __syncwarp(); if (lane == 0) mbar_arrive(&cb_empty[s]); sum += __uint_as_float(v[0]) + __uint_as_float(v[63]); continue; }
+        // x = S + colbias on packed fp32 pairs (FADD2: two lanes' worth of adds per instruction)
         const float4* cbt = reinterpret_cast<const float4*>(sCb + s * 128 + half * 64);
-        float* x = reinterpret_cast<float*>(v);
-        float mx[4];
+        float2 x2[32];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const float4 c4 = cbt[q];
-          x[4 * q + 0] = __uint_as_float(v[4 * q + 0]) + c4.x;
-          x[4 * q + 1] = __uint_as_float(v[4 * q + 1]) + c4.y;
-          x[4 * q + 2] = __uint_as_float(v[4 * q + 2]) + c4.z;
-          x[4 * q + 3] = __uint_as_float(v[4 * q + 3]) + c4.w;
-          // 4 independent 3-input max chains (FMNMX3), tree-combined below
-          const int c = q & 3;
-          mx[c] = (q < 4) ? fmaxf(x[4 * q], fmaxf(x[4 * q + 1], fmaxf(x[4 * q + 2], x[4 * q + 3])))
-                          : fmaxf(mx[c], fmaxf(fmaxf(x[4 * q], x[4 * q + 1]), fmaxf(x[4 * q + 2], x[4 * q + 3])));
+          x2[2 * q] = __fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])), make_float2(c4.x, c4.y));
+          x2[2 * q + 1] = __fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])), make_float2(c4.z, c4.w));
         }
-        const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         __syncwarp();
         if (lane == 0) mbar_arrive(&cb_empty[s]);
-        if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
-          sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
-          mref = tmax;
-        }
-        if (mref > -INFINITY) {
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        // row max of this tile half (4 independent 3-input max chains, FMNMX3)
+        auto tile_max = [&]() {
+          float mx[4];
 #pragma unroll
-          for (int k = 0; k < 64; k += 4) {
-            s0 += ex2(x[k] - mref);
-            s1 += ex2(x[k + 1] - mref);
-            s2 += ex2(x[k + 2] - mref);
-            s3 += ex2(x[k + 3] - mref);
+          for (int q = 0; q < 16; ++q) {
+            const int c = q & 3;
+            const float m4 = fmaxf(fmaxf(x2[2 * q].x, x2[2 * q].y), fmaxf(x2[2 * q + 1].x, x2[2 * q + 1].y));
+            mx[c] = (q < 4) ? m4 : fmaxf(mx[c], m4);
           }
-          sum += (s0 + s1) + (s2 + s3);
+          return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        };
+        auto tile_sum = [&](float m) {
+          // NPOLY of every 16 exponentials run on the FMA pipe (ex2_poly), the rest on MUFU;
+          // arguments and partial sums on packed pairs (4 independent float2 accumulators)
+          const float2 nm = make_float2(-m, -m);
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float2 y = __fadd2_rn(x2[q], nm);
+            const int k = 2 * q;
+            const float e0 = ((k & 15) >= 16 - NPOLY) ? ex2_poly(y.x) : ex2(y.x);
+            const float e1 = (((k + 1) & 15) >= 16 - NPOLY) ? ex2_poly(y.y) : ex2(y.y);
+            acc[q & 3] = __fadd2_rn(acc[q & 3], make_float2(e0, e1));
+          }
+          const float2 t01 = __fadd2_rn(acc[0], acc[1]), t23 = __fadd2_rn(acc[2], acc[3]);
+          const float2 tt = __fadd2_rn(t01, t23);
+          return tt.x + tt.y;
+        };
+        if constexpr (MAXFREE) {
+          // Optimistic reference: the row's reference mref is the exact max of the first tile with
+          // a finite value and is only raised when a later tile's partial sum leaves the safe range
+          // (overflow / NaN from an argument >= 128): then the tile is redone against its own max.
+          // The first tile contributes ex2(0) = 1, so anything underflowing below it is negligible.
+          if (mref == -INFINITY) mref = tile_max();
+          if (mref > -INFINITY) {
+            float ts = tile_sum(mref);
+            if (!(ts <= 1.0e30f)) {
+              const float tmax = tile_max();
+              sum *= ex2(mref - tmax);
+              mref = tmax;
+              ts = tile_sum(mref);
+            }
+            sum += ts;
+          }
+        } else {
+          const float tmax = tile_max();
+          if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
+            sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
+            mref = tmax;
+          }
+          if (mref > -INFINITY) sum += tile_sum(mref);
         }
       }
       // merge the two column halves of each row (half 1 -> SMEM -> half 0)
@@ -618,7 +670,6 @@ struct BGeo {
   static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
   static constexpr int SMW = 8;                                // softmax warps
   static constexpr int THREADS = 64 + 32 * SMW;
-  static constexpr int GCOL = 256;                             // TMEM column of the gradient accumulator
   static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 2 * 128 * 4 + 512;
 };
 
@@ -631,9 +682,10 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
@@ -671,6 +723,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   constexpr uint32_t GN = PACKED ? 4 * D : 2 * D;            // N of the gradient MMA
   constexpr bool PLO = (GT == 3 || GT == 5);                 // P~ lo part needed
   constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | (GN >> 3 << 17) | ((128u >> 4) << 24);
+  // S/P~ TMEM buffers (128 columns each) ahead of the gradient accumulator: three when the
+  // accumulator fits in the last 128 columns, so S(j+1) never waits for the gradient GEMM of j-1.
+  constexpr int NSB = (GN <= 128) ? 3 : 2;
+  constexpr uint32_t GCOL = NSB * 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sO = smem;
@@ -684,12 +740,12 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   uint64_t* t_empty = bars + 2 + ST;        // [ST]
   uint64_t* h_full = bars + 2 + 2 * ST;     // [ST]
   uint64_t* h_empty = bars + 2 + 3 * ST;    // [ST]
-  uint64_t* s_full = bars + 2 + 4 * ST;     // [2]  S tile ready in TMEM buffer
-  uint64_t* s_empty = bars + 4 + 4 * ST;    // [2]  buffer free (its P~ consumed by the gradient GEMM)
-  uint64_t* p_full = bars + 6 + 4 * ST;     // [2]  P~ written back into the buffer
-  uint64_t* g_full = bars + 8 + 4 * ST;
-  uint64_t* g_empty = bars + 9 + 4 * ST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 4 * ST);
+  uint64_t* s_full = bars + 2 + 4 * ST;     // [3]  S tile ready in TMEM buffer
+  uint64_t* s_empty = bars + 5 + 4 * ST;    // [3]  buffer free (its P~ consumed by the gradient GEMM)
+  uint64_t* p_full = bars + 8 + 4 * ST;     // [3]  P~ written back into the buffer
+  uint64_t* g_full = bars + 11 + 4 * ST;
+  uint64_t* g_empty = bars + 12 + 4 * ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 4 * ST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int units = a.B * a.o_tiles;
@@ -700,7 +756,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
       mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], G::SMW);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], G::SMW); }
+    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], G::SMW); }
     mbar_init(g_full, 1); mbar_init(g_empty, G::SMW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -737,13 +793,13 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     TMC_PROF_END(lane == 0, 14, _tr0);
   } else if (warp == 1) {
     TMC_PROF_T0(_tr1);
-    if (lane == 0) {   // ---------------- MMA issuer
+    {   // ---------------- MMA issuer (whole warp, one elected lane issues)
       uint32_t t = 0, ua = 0;
       const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
       auto grad = [&](uint32_t tt, bool first) {
-        const uint32_t as = tt & 1;
-        TMC_PROF_WAIT(true, 5, mbar_wait(&p_full[as], (tt >> 1) & 1));
-        if (first) TMC_PROF_WAIT(true, 7, mbar_wait(g_empty, (ua & 1) ^ 1));
+        const uint32_t as = tt % NSB;
+        TMC_PROF_WAIT(lane == 0, 5, mbar_wait(&p_full[as], (tt / NSB) & 1));
+        if (first) TMC_PROF_WAIT(lane == 0, 7, mbar_wait(g_empty, (ua & 1) ^ 1));
         tc_fence_after();
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
         const uint32_t pA = tmem + as * 128;
@@ -754,23 +810,23 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
           const uint32_t acc0 = (!first || kk) ? 1u : 0u;
           if constexpr (PACKED) {
-            if constexpr (GT == 5) mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, acc0);
-            mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, GT == 5 ? 1u : acc0);
+            if constexpr (GT == 5) mma_f16_ts(tmem + GCOL, plo, thi, IDESC_G, acc0);
+            mma_f16_ts(tmem + GCOL, phi, thi, IDESC_G, GT == 5 ? 1u : acc0);
           } else {
-            if constexpr (GT >= 3) mma_f16_ts(tmem + G::GCOL, plo, thi, IDESC_G, acc0);
-            if constexpr (GT >= 2) mma_f16_ts(tmem + G::GCOL, phi, tlo, IDESC_G, GT >= 3 ? 1u : acc0);
-            mma_f16_ts(tmem + G::GCOL, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
+            if constexpr (GT >= 3) mma_f16_ts(tmem + GCOL, plo, thi, IDESC_G, acc0);
+            if constexpr (GT >= 2) mma_f16_ts(tmem + GCOL, phi, tlo, IDESC_G, GT >= 3 ? 1u : acc0);
+            mma_f16_ts(tmem + GCOL, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
           }
         }
         mma_commit(&t_empty[tt % ST]);
         mma_commit(&s_empty[as]);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        TMC_PROF_WAIT(true, 6, mbar_wait(o_full, ua & 1));
+        TMC_PROF_WAIT(lane == 0, 6, mbar_wait(o_full, ua & 1));
         for (int j = 0; j < a.t_tiles; ++j, ++t) {
-          const int s = t % ST, as = t & 1;
-          TMC_PROF_WAIT(true, 3, mbar_wait(&t_full[s], (t / ST) & 1));
-          TMC_PROF_WAIT(true, 4, mbar_wait(&s_empty[as], ((t >> 1) & 1) ^ 1));
+          const int s = t % ST, as = t % NSB;
+          TMC_PROF_WAIT(lane == 0, 3, mbar_wait(&t_full[s], (t / ST) & 1));
+          TMC_PROF_WAIT(lane == 0, 4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
 #pragma unroll
@@ -814,8 +870,8 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
       float rsum = 0.f;
       for (int j = 0; j < a.t_tiles; ++j, ++t) {
-        const int as = t & 1, s = t % ST;
-        TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t >> 1) & 1));
+        const int as = t % NSB, s = t % ST;
+        TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
         uint32_t v[64];
         const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + half * 64);
@@ -868,7 +924,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       {
         uint32_t* r0 = reinterpret_cast<uint32_t*>(g0);
         uint32_t* r1 = reinterpret_cast<uint32_t*>(g1);
-        const uint32_t gaddr = tmem + lane_off + (uint32_t)G::GCOL + half * DH;
+        const uint32_t gaddr = tmem + lane_off + GCOL + half * DH;
         if constexpr (DH == 16) {
           TMC_LD16(gaddr, r0);
           TMC_LD16(gaddr + D, r1);
@@ -1086,12 +1142,21 @@ inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in,
   return 1;
 }
 
-template <int D>
-inline void tc_fwd_launch(const tc::FwdArgs& f, cudaStream_t s) {
+// Forward softmax variant (TMC_FWD_VARIANT overrides):
+//   0 = tile max + lazy rescale, 1 = optimistic reference (no per-tile max), 2 = 1 + 2/16 polynomial exps.
+constexpr int kDefaultFwdVariant = 0;
+inline int tc_fwd_variant() {
+  const char* e = std::getenv("TMC_FWD_VARIANT");
+  const int v = e ? std::atoi(e) : kDefaultFwdVariant;
+  return (v >= 0 && v <= 2) ? v : kDefaultFwdVariant;
+}
+
+template <int D, int NPOLY, bool MF>
+inline void tc_fwd_launch_t(const tc::FwdArgs& f, cudaStream_t s) {
   using G = tc::Geo<D>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc::tc_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaFuncSetAttribute(tc::tc_fwd_kernel<D, NPOLY, MF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     attr = true;
   }
   static int sms = 0;
@@ -1102,7 +1167,16 @@ inline void tc_fwd_launch(const tc::FwdArgs& f, cudaStream_t s) {
   }
   const int units = f.B * (f.a_tiles / G::RB);
   const int grid = units < sms ? units : sms;
-  tc::tc_fwd_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
+  tc::tc_fwd_kernel<D, NPOLY, MF><<<grid, G::THREADS, G::SMEM, s>>>(f);
+}
+
+template <int D>
+inline void tc_fwd_launch(const tc::FwdArgs& f, cudaStream_t s) {
+  switch (tc_fwd_variant()) {
+    case 1: return tc_fwd_launch_t<D, 0, true>(f, s);
+    case 2: return tc_fwd_launch_t<D, 2, true>(f, s);
+    default: return tc_fwd_launch_t<D, 0, false>(f, s);
+  }
 }
 
 // Forward contraction of one edge on tensor cores.  zrows = DOWN (rows = z side).

@@ -20,9 +20,11 @@ grads = tmc.alloc_grads(g)
 s = torch.cuda.current_stream()
 pairs = B * sum(wl.K[i] * wl.Kp(i) for i in range(len(wl.parent)) if wl.parent[i] >= 0)
 for st in settings:
-    flags, gt = st.split(":")
+    parts = st.split(":") + ["0"] * 3
+    flags, gt, poly = parts[0], parts[1] or "3", parts[2] or "0"
     os.environ["TMC_DEBUG_FLAGS"] = flags
     os.environ["TMC_BWD_GRAD_TERMS"] = gt
+    os.environ["TMC_FWD_VARIANT"] = poly
     for _ in range(2):
         tmc.tmc_forward(g, inp, logp, ws, None, s); tmc.tmc_backward(g, inp, ws, None, grads, None, None, s)
     torch.cuda.synchronize()
@@ -37,5 +39,5 @@ for st in settings:
     e[2].record(s)
     torch.cuda.synchronize()
     fwd, bwd = e[0].elapsed_time(e[1]) / n, e[1].elapsed_time(e[2]) / n
-    print(json.dumps({"cfg": cfg_name, "B": B, "flags": int(flags), "grad_terms": int(gt), "fwd_ms": fwd, "bwd_ms": bwd,
+    print(json.dumps({"cfg": cfg_name, "B": B, "flags": int(flags), "grad_terms": int(gt), "fwd_variant": int(poly), "fwd_ms": fwd, "bwd_ms": bwd,
                       "fwd_pairs_per_clk_sm": pairs / (fwd * 1e-3) / 148 / 1.965e9}), flush=True)

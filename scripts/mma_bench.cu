@@ -1,0 +1,101 @@
+// tcgen05.mma issue-rate microbenchmark on B200 (sm_100a): cycles per instruction for the MMA
+// shapes the TMC kernels use.  One CTA per SM, one elected thread issues N back-to-back MMAs into
+// TMEM (operands: a 128x64 fp16 SWIZZLE_128B K-major tile pair in shared memory, or A from TMEM),
+// then commits and waits; the kernel reports clock64 cycles / N.  Prints one JSON line.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/mma_bench scripts/mma_bench.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+template <int MODE>   // 0: SS K-major N=128; 1: SS N=64; 2: TS (A in TMEM) B MN-major N=64; 3: TS N=128; 4: SS N=256
+__global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    const uint32_t A = smem_u32(smem), Bs = A + 32768;
+    constexpr uint32_t N = (MODE == 1 || MODE == 2) ? 64 : (MODE == 4 ? 256 : 128);
+    constexpr uint32_t bmaj = (MODE >= 2 && MODE <= 3) ? 1u : 0u;
+    constexpr uint32_t idesc = (1u << 4) | (bmaj << 16) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const uint32_t acc = i ? 1u : 0u;
+      const uint32_t koff = (i & 3) * 32;
+      if constexpr (MODE <= 1 || MODE == 4) {
+        const uint64_t a = sdesc(A + koff), b = sdesc(Bs + koff);
+        asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                     "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      } else {
+        const uint64_t b = sdesc_mn(Bs + (i & 7) * 2048, 16384);
+        asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                     "r"(tmem + (i & 7) * 8), "l"(b), "r"(idesc), "r"(acc));
+      }
+    }
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(&bar))
+                 : "memory");
+    asm volatile("{\n.reg .pred P1;\nW: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(
+        smem_u32(&bar)));
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int MODE>
+double run(int sms, unsigned long long* d, unsigned long long* h, int n) {
+  cudaFuncSetAttribute(bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
+  bench<MODE><<<sms, 128, 70 * 1024>>>(n, d);
+  bench<MODE><<<sms, 128, 70 * 1024>>>(n, d);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+  double s = 0;
+  for (int i = 0; i < sms; ++i) s += h[i];
+  return s / sms / n;
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unsigned long long *d, h[1024];
+  cudaMalloc(&d, sizeof(h));
+  const int n = 4096;
+  printf("{\"clk_per_mma_ss_n128\": %.1f, \"clk_per_mma_ss_n64\": %.1f, \"clk_per_mma_ts_mn_n64\": %.1f, "
+         "\"clk_per_mma_ts_mn_n128\": %.1f, \"clk_per_mma_ss_n256\": %.1f, \"err\": \"%s\"}\n",
+         run<0>(sms, d, h, n), run<1>(sms, d, h, n), run<2>(sms, d, h, n), run<3>(sms, d, h, n), run<4>(sms, d, h, n),
+         cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

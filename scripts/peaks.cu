@@ -66,6 +66,21 @@ __global__ void k_fmax(float* out, float seed) {
   if (s == 1234.5f) out[0] = s;
 }
 
+__global__ void k_fadd2(float* out, float seed) {
+  float2 a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = make_float2(seed * (threadIdx.x + j), seed * j);
+  const float2 c = make_float2(seed * 1e-3f, seed * 2e-3f);
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __fadd2_rn(a[j], c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
+  if (s == 1234.5f) out[0] = s;
+}
+
 // mixed: what the forward softmax does per pair (FADD bias, FMNMX, FFMA-folded subtract in ex2 arg, FADD sum)
 __global__ void k_mixed(float* out, float seed) {
   float x[8], s[8];
@@ -118,13 +133,13 @@ int main() {
   const double ghz = clk_khz * 1e-6;
   auto rate = [&](float ms) { return ops / (ms * 1e-3); };
   float t_ex2 = run(k_ex2, sms, out), t_ffma = run(k_ffma, sms, out), t_fadd = run(k_fadd, sms, out),
-        t_fmax = run(k_fmax, sms, out), t_mixed = run(k_mixed, sms, out);
+        t_fmax = run(k_fmax, sms, out), t_mixed = run(k_mixed, sms, out), t_fadd2 = run(k_fadd2, sms, out);
   printf("{\"sms\": %d, \"clock_attr_ghz\": %.3f, "
          "\"ex2_per_s\": %.4e, \"ffma_per_s\": %.4e, \"fadd_per_s\": %.4e, \"fmax_per_s\": %.4e, "
-         "\"mixed_pairs_per_s\": %.4e, "
+         "\"mixed_pairs_per_s\": %.4e, \"fadd2_lanes_per_clk_sm_at_attr\": %.2f, "
          "\"ex2_per_clk_sm_at_attr\": %.2f, \"ffma_per_clk_sm_at_attr\": %.2f, \"fadd_per_clk_sm_at_attr\": %.2f, "
          "\"fmax_per_clk_sm_at_attr\": %.2f, \"mixed_pairs_per_clk_sm_at_attr\": %.2f}\n",
-         sms, ghz, rate(t_ex2), rate(t_ffma), rate(t_fadd), rate(t_fmax), rate(t_mixed),
+         sms, ghz, rate(t_ex2), rate(t_ffma), rate(t_fadd), rate(t_fmax), rate(t_mixed), 2 * rate(t_fadd2) / sms / (ghz * 1e9),
          rate(t_ex2) / sms / (ghz * 1e9), rate(t_ffma) / sms / (ghz * 1e9), rate(t_fadd) / sms / (ghz * 1e9),
          rate(t_fmax) / sms / (ghz * 1e9), rate(t_mixed) / sms / (ghz * 1e9));
   return 0;
