@@ -45,8 +45,8 @@ struct Geo {
   static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS;
   static constexpr int TMEM_COLS = RB * 2 * 128;
   static constexpr size_t SMEM = 1024 /*align*/ + (size_t)RB * TILE + (size_t)STAGES * TILE +
-                                 (size_t)STAGES * 128 * 4 + (size_t)RB * 128 * 8 /*half merge*/ +
-                                 512 /*barriers*/;
+                                 (size_t)(STAGES + 1) * 4096 /*bias operand ring + constant ones*/ +
+                                 (size_t)RB * 128 * 8 /*half merge*/ + 512 /*barriers*/;
 };
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -78,7 +78,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Optional instrumentation (-DTMC_INSTRUMENT builds libtmc_instr.so only): cycles each role spends
 // waiting on each barrier, per CTA, read back with tmc_debug_counters().
 #ifdef TMC_INSTRUMENT
-__device__ unsigned long long g_tmc_prof[1024][16];
+__device__ unsigned long long g_tmc_prof[1024][32];
 #define TMC_PROF_WAIT(cond, slot, call)                                                   \
   do {                                                                                    \
     const long long _t0 = clock64();                                                      \
@@ -99,6 +99,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -171,6 +172,19 @@ __host__ __device__ __forceinline__ uint32_t swz_off(int r, int k) {
   const int atom = k >> 6, kk = k & 63;
   const int chunk = (kk >> 3) ^ (r & 7);
   return (uint32_t)(atom * kAtomBytes + r * 128 + chunk * 16 + (kk & 7) * 2);
+}
+
+// Extra K=16 operand of the forward (column bias on the tensor core): 128 rows x 16 fp16, K-major,
+// no swizzle, 8-row x 16-byte core matrices: (row r, k) at (r/8)*256 + (k/8)*128 + (r%8)*16 + (k%8)*2.
+constexpr int kBxBytes = 128 * 16 * 2;
+__host__ __device__ __forceinline__ uint32_t bx_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 256 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+// K-major SWIZZLE_NONE descriptor for that layout: LBO = 128 B (next core matrix along K),
+// SBO = 256 B (next 8-row group), version 1.
+__device__ __forceinline__ uint64_t sdesc_bx(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46);
 }
 
 // ------------------------------------------------------------------------------ K1: operand prep
@@ -343,6 +357,7 @@ struct ColbiasArgs {
   int betaStride;
   int C, Cpad;
   float* cb2;            // [B][Cpad] out: (cb + beta - cbmax) * log2e, -inf padded
+  uint8_t* bx;           // [B][Cpad/128][kBxBytes] out: the same bias as an extra K=16 MMA operand, or NULL
   float* cbmax;          // [B]
   const double *off_cb, *off_rb;
   double* off_out;
@@ -373,6 +388,19 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
       v *= kLog2E;
     }
     a.cb2[(size_t)b * a.Cpad + c] = v;
+    if (a.bx) {
+      // row c of the extra operand: k = 0 -> fp16 hi, k = 1 -> fp16 lo of the bias (the constant A
+      // operand has ones there), so the tensor core adds the column bias to S exactly to ~2^-22.
+      // Biases below -60000 (log2 units) contribute exactly 0 anyway; clamp so hi/lo stay finite.
+      const float vc = fmaxf(v, -60000.f);
+      __half hh, ll;
+      split16(vc, hh, ll);
+      uint8_t* tile = a.bx + ((size_t)b * (a.Cpad / kTileRows) + c / kTileRows) * kBxBytes;
+      const int r = c % kTileRows;
+      const uint32_t w0 = (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
+      *reinterpret_cast<uint4*>(tile + bx_off(r, 0)) = make_uint4(w0, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(tile + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   if (tid == 0) {
     a.cbmax[b] = cmax;
@@ -388,6 +416,7 @@ struct FwdArgs {
   const uint8_t *At, *Bt;      // row / column operand tile images [B][tiles][TILE]
   int a_tiles, b_tiles;        // 128-row tiles per datapoint (a_tiles multiple of RB)
   const float* cb2;            // [B][b_tiles*128]
+  const uint8_t* Bx;           // [B][b_tiles][kBxBytes] column bias as the extra K=16 MMA operand
   const float* ell_add;        // [B][ell_stride] added to ell (UP: beta of the row/param side) or NULL
   int ell_stride;
   const float* out_add;        // [B][R] added to out (DOWN: unary of the row/z side) or NULL
@@ -405,8 +434,9 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared window
   uint8_t* sA = smem;                                   // RB tiles
   uint8_t* sB = sA + (size_t)RB * G::TILE;              // ST tiles
-  float* sCb = reinterpret_cast<float*>(sB + (size_t)ST * G::TILE);   // ST x 128
-  float2* sMerge = reinterpret_cast<float2*>(sCb + ST * 128);          // RB x 128 (max, sum) of half 1
+  uint8_t* sBx = sB + (size_t)ST * G::TILE;                            // ST x kBxBytes (bias operand ring)
+  uint8_t* sAx = sBx + (size_t)ST * kBxBytes;                          // constant ones operand
+  float2* sMerge = reinterpret_cast<float2*>(sAx + kBxBytes);          // RB x 128 (max, sum) of half 1
   uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + RB * 128);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 1;
@@ -434,7 +464,13 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], G::SOFTMAX_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  // constant A operand of the bias MMA: k = 0, 1 are ones (times the bias hi and lo parts)
+  for (int r = tid; r < kTileRows; r += blockDim.x) {
+    *reinterpret_cast<uint4*>(sAx + bx_off(r, 0)) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sAx + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async();
+  if (warp == G::SOFTMAX_WARPS + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(G::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -444,7 +480,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == G::SOFTMAX_WARPS) {
     TMC_PROF_T0(_tr0);
     // ===================== producer: bulk copies (TMA engine) =====================
     if (lane == 0) {
@@ -458,21 +494,19 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
           TMC_PROF_WAIT(true, 0, mbar_wait(&b_empty[s], ph));
-          mbar_expect_tx(&b_full[s], G::TILE);
+          mbar_expect_tx(&b_full[s], G::TILE + kBxBytes);
           bulk_g2s(sB + (size_t)s * G::TILE, a.Bt + ((size_t)b * a.b_tiles + j) * G::TILE, G::TILE, &b_full[s]);
-          TMC_PROF_WAIT(true, 1, mbar_wait(&cb_empty[s], ph));
-          mbar_expect_tx(&cb_full[s], 512);
-          bulk_g2s(sCb + s * 128, a.cb2 + ((size_t)b * a.b_tiles + j) * 128, 512, &cb_full[s]);
+          bulk_g2s(sBx + (size_t)s * kBxBytes, a.Bx + ((size_t)b * a.b_tiles + j) * kBxBytes, kBxBytes, &b_full[s]);
         }
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
-  } else if (warp == 1) {
+  } else if (warp == G::SOFTMAX_WARPS + 1) {
     TMC_PROF_T0(_tr1);
     // ===================== MMA issuer (whole warp, one elected lane issues) =====================
     {
       uint32_t t = 0, ua = 0;
-      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB), axBase = smem_u32(sAx), bxBase = smem_u32(sBx);
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         TMC_PROF_WAIT(lane == 0, 6, mbar_wait(a_full, ua & 1));
         for (int j = 0; j < a.b_tiles; ++j, ++t) {
@@ -504,6 +538,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
                 mma_f16(d, sdesc(A + o), sdesc(Bs + o), kIdescF16M128N128, 1u);
               }
             }
+            // + column bias: ones(128 x 16) . [cb_hi, cb_lo, 0..]^T
+            mma_f16(d, sdesc_bx(axBase), sdesc_bx(bxBase + s * kBxBytes), kIdescF16M128N128, 1u);
           }
           mma_commit(&b_empty[s]);
           mma_commit(&acc_full[as]);
@@ -517,7 +553,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     // ===================== softmax warps: TMEM -> online log2-sum-exp2 =====================
     // warp -> (TMEM lane quarter, row block rb, column half): each thread owns one row of one
     // 64-column half of every S tile; the two halves' (max, sum) states merge at the unit's end.
-    const int sw = warp - 2;
+    const int sw = warp;
     const int rb = (sw >> 2) % RB;
     const int half = sw / (4 * RB);
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
@@ -538,19 +574,11 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[as]);
-        TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&cb_full[s], (t / ST) & 1));
-        if (a.dbg & 2) { __syncwarp(); if (lane == 0) mbar_arrive(&cb_empty[s]); sum += __uint_as_float(v[0]) + __uint_as_float(v[63]); continue; }
-        // x = S + colbias on packed fp32 pairs (FADD2: two lanes' worth of adds per instruction)
-        const float4* cbt = reinterpret_cast<const float4*>(sCb + s * 128 + half * 64);
+        if (a.dbg & 2) { sum += __uint_as_float(v[0]) + __uint_as_float(v[63]); continue; }
+        // x = S + colbias, both from the tensor core (the bias is the extra K=16 MMA)
         float2 x2[32];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 c4 = cbt[q];
-          x2[2 * q] = __fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])), make_float2(c4.x, c4.y));
-          x2[2 * q + 1] = __fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])), make_float2(c4.z, c4.w));
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&cb_empty[s]);
+        for (int q = 0; q < 32; ++q) x2[q] = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
         // row max of this tile half (4 independent 3-input max chains, FMNMX3)
         auto tile_max = [&]() {
           float mx[4];
@@ -623,11 +651,11 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
       }
       named_bar(1, 32 * G::SOFTMAX_WARPS);   // sMerge is reused by the next unit
     }
-    TMC_PROF_END(warp == 2 && lane == 0, 13, _tr2);
+    TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == G::SOFTMAX_WARPS + 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::TMEM_COLS));
   }
@@ -668,9 +696,9 @@ struct BGeo {
   static constexpr int PART = Geo<D>::PART;
   static constexpr int ATOMS = Geo<D>::ATOMS;
   static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
-  static constexpr int SMW = 8;                                // softmax warps
+  static constexpr int SMW = 16;                               // softmax warps (4 per TMEM lane quarter)
   static constexpr int THREADS = 64 + 32 * SMW;
-  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 2 * 128 * 4 + 512;
+  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 4 * 128 * 4 + 512;
 };
 
 // MN-major SWIZZLE_128B descriptor: LBO = stride of 64-element MN chunks, SBO = 8-row K groups.
@@ -699,6 +727,18 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),   \
       "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                                                    \
       : "memory")
+
+#define TMC_ST16(taddr, v)                                                                                          \
+  asm volatile(                                                                                                     \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"      \
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),         \
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])                 \
+      : "memory")
+
+#define TMC_LD8(taddr, v)                                                                                           \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                             \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])    \
+               : "r"(taddr))
 
 #define TMC_LD16(taddr, v)                                                                                          \
   asm volatile(                                                                                                     \
@@ -732,8 +772,8 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   uint8_t* sO = smem;
   uint8_t* sT = sO + G::TILE;
   float* sHt = reinterpret_cast<float*>(sT + (size_t)ST * G::TILE);
-  float* sRs = sHt + ST * 128;                              // [2 (unit parity)][2 (half)][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRs + 512);
+  float* sRs = sHt + ST * 128;                              // [2 (unit parity)][4 (column quarter)][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRs + 1024);
   uint64_t* o_full = bars + 0;
   uint64_t* o_empty = bars + 1;
   uint64_t* t_full = bars + 2;              // [ST]
@@ -760,7 +800,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     mbar_init(g_full, 1); mbar_init(g_empty, G::SMW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == G::SMW + 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -769,7 +809,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == G::SMW) {
     TMC_PROF_T0(_tr0);
     if (lane == 0) {   // ---------------- producer
       uint32_t t = 0, ua = 0;
@@ -791,7 +831,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
-  } else if (warp == 1) {
+  } else if (warp == G::SMW + 1) {
     TMC_PROF_T0(_tr1);
     {   // ---------------- MMA issuer (whole warp, one elected lane issues)
       uint32_t t = 0, ua = 0;
@@ -803,10 +843,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         tc_fence_after();
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
         const uint32_t pA = tmem + as * 128;
+        TMC_PROF_T0(_tg);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (a.dbg & 2) break;
-          const uint32_t phi = pA + (kk >> 2) * 64 + (kk & 3) * 8, plo = phi + 32;
+          const uint32_t phi = pA + (kk >> 1) * 32 + (kk & 1) * 8, plo = phi + 16;
           const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
           const uint32_t acc0 = (!first || kk) ? 1u : 0u;
           if constexpr (PACKED) {
@@ -818,8 +859,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
             mma_f16_ts(tmem + GCOL, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
           }
         }
+        TMC_PROF_END(lane == 0, 11, _tg);
+        TMC_PROF_T0(_tc);
         mma_commit(&t_empty[tt % ST]);
         mma_commit(&s_empty[as]);
+        TMC_PROF_END(lane == 0, 16, _tc);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         TMC_PROF_WAIT(lane == 0, 6, mbar_wait(o_full, ua & 1));
@@ -827,8 +871,9 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           const int s = t % ST, as = t % NSB;
           TMC_PROF_WAIT(lane == 0, 3, mbar_wait(&t_full[s], (t / ST) & 1));
           TMC_PROF_WAIT(lane == 0, 4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
-          tc_fence_after();
+          TMC_PROF_WAIT(lane == 0, 17, tc_fence_after());
           const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
+          TMC_PROF_T0(_ts);
 #pragma unroll
           for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
 #pragma unroll
@@ -846,7 +891,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
               mma_f16(d, sdesc(oBase + o), sdesc(Ts + o), IDESC_S, 1u);
             }
           }
+          TMC_PROF_END(lane == 0, 15, _ts);
+          TMC_PROF_T0(_tc2);
           mma_commit(&s_full[as]);
+          TMC_PROF_END(lane == 0, 18, _tc2);
           if (j > 0) grad(t - 1, j == 1);
         }
         grad(t - 1, a.t_tiles == 1);
@@ -857,10 +905,13 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     TMC_PROF_END(lane == 0, 12, _tr1);
   } else {
     TMC_PROF_T0(_tr2);
-    // ---------------- softmax / P~ warps (8) + epilogue
-    const int sw = warp - 2;
+    // ---------------- softmax / P~ warps (16) + epilogue
+    // warp -> (TMEM lane quarter, column quarter cq): 32 columns of every S tile; P~ hi/lo go back
+    // into those same 32 columns (hi in the first 16, lo in the last 16), so no warp writes TMEM
+    // columns another warp still has to read.
+    const int sw = warp;
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
-    const int half = sw >> 2;                   // 64-column half of the tile (and half of the dims)
+    const int cq = sw >> 2;                     // column quarter of the tile (and quarter of the dims)
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
@@ -868,82 +919,84 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       const int b = u / a.o_tiles, mt = u % a.o_tiles;
       const int gm = mt * 128 + m;
       const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
-      float rsum = 0.f;
+      const float2 hom2 = make_float2(hom, hom);
+      float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       for (int j = 0; j < a.t_tiles; ++j, ++t) {
         const int as = t % NSB, s = t % ST;
         TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
-        uint32_t v[64];
-        const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + half * 64);
-        TMC_LD32(taddr + 0, (v + 0));
-        TMC_LD32(taddr + 32, (v + 32));
+        uint32_t v[32];
+        const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
+        TMC_LD32(taddr, v);
         tmem_ld_wait();
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
-        const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + half * 64);
-        uint32_t hi[32], lo[32];
+        const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
+        uint32_t hi[16], lo[16];
         if (hom > -INFINITY && !(a.dbg & 4)) {
-          float r0 = 0.f, r1 = 0.f;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const float4 h4 = hts[q];
-            const float p0 = ex2(__uint_as_float(v[4 * q + 0]) + h4.x + hom);
-            const float p1 = ex2(__uint_as_float(v[4 * q + 1]) + h4.y + hom);
-            const float p2 = ex2(__uint_as_float(v[4 * q + 2]) + h4.z + hom);
-            const float p3 = ex2(__uint_as_float(v[4 * q + 3]) + h4.w + hom);
-            r0 += p0 + p1;
-            r1 += p2 + p3;
-            __half2 h01 = __floats2half2_rn(p0, p1), h23 = __floats2half2_rn(p2, p3);
+            // arguments on packed pairs: S + ht + (ho + 14)
+            const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
+                                                     make_float2(h4.x, h4.y)), hom2);
+            const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
+                                                     make_float2(h4.z, h4.w)), hom2);
+            const float2 p01 = make_float2(ex2(y01.x), ex2(y01.y)), p23 = make_float2(ex2(y23.x), ex2(y23.y));
+            racc[0] = __fadd2_rn(racc[0], p01);
+            racc[1] = __fadd2_rn(racc[1], p23);
+            __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
             hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
             hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
             if constexpr (PLO) {
               const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-              __half2 l01 = __floats2half2_rn(p0 - f01.x, p1 - f01.y), l23 = __floats2half2_rn(p2 - f23.x, p3 - f23.y);
+              const float2 d01 = __fadd2_rn(p01, make_float2(-f01.x, -f01.y));
+              const float2 d23 = __fadd2_rn(p23, make_float2(-f23.x, -f23.y));
+              __half2 l01 = __floats2half2_rn(d01.x, d01.y), l23 = __floats2half2_rn(d23.x, d23.y);
               lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
               lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
             }
           }
-          rsum += r0 + r1;
         } else {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) { hi[q] = 0u; lo[q] = 0u; }
+          for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
-        TMC_ST32(taddr, hi);
-        if constexpr (PLO) TMC_ST32(taddr + 32, lo);
+        TMC_ST16(taddr, hi);
+        if constexpr (PLO) TMC_ST16(taddr + 16, lo);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
       }
-      // ---------------- epilogue: G -> gradients (this warp: dims [half*D/2, (half+1)*D/2))
-      constexpr int DH = D / 2;
+      // ---------------- epilogue: G -> gradients (this warp: dims [cq*D/4, (cq+1)*D/4))
+      constexpr int DQ = D / 4;
       TMC_PROF_WAIT(sw == 0 && lane == 0, 10, mbar_wait(g_full, ua & 1));
       tc_fence_after();
-      float g0[DH], g1[DH];          // G[:, d] and G[:, D + d] for this warp's dims
+      float g0[DQ], g1[DQ];          // G[:, d] and G[:, D + d] for this warp's dims
       {
         uint32_t* r0 = reinterpret_cast<uint32_t*>(g0);
         uint32_t* r1 = reinterpret_cast<uint32_t*>(g1);
-        const uint32_t gaddr = tmem + lane_off + GCOL + half * DH;
-        if constexpr (DH == 16) {
+        const uint32_t gaddr = tmem + lane_off + GCOL + cq * DQ;
+        if constexpr (DQ == 8) {
+          TMC_LD8(gaddr, r0);
+          TMC_LD8(gaddr + D, r1);
+        } else {
           TMC_LD16(gaddr, r0);
           TMC_LD16(gaddr + D, r1);
-        } else {
-          TMC_LD32(gaddr, r0);
-          TMC_LD32(gaddr + D, r1);
         }
         if constexpr (PACKED) {     // + the T_lo column half
-          uint32_t q0[DH], q1[DH];
-          if constexpr (DH == 16) {
+          uint32_t q0[DQ], q1[DQ];
+          if constexpr (DQ == 8) {
+            TMC_LD8(gaddr + 2 * D, q0);
+            TMC_LD8(gaddr + 3 * D, q1);
+          } else {
             TMC_LD16(gaddr + 2 * D, q0);
             TMC_LD16(gaddr + 3 * D, q1);
-          } else {
-            TMC_LD32(gaddr + 2 * D, q0);
-            TMC_LD32(gaddr + 3 * D, q1);
           }
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < DH; ++e) {
+          for (int e = 0; e < DQ; ++e) {
             g0[e] += __uint_as_float(q0[e]);
             g1[e] += __uint_as_float(q1[e]);
           }
@@ -953,20 +1006,21 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(g_empty);
-      float* rs = sRs + (ua & 1) * 256;
-      rs[half * 128 + m] = rsum;
+      float* rs = sRs + (ua & 1) * 512;
+      const float2 rr = __fadd2_rn(racc[0], racc[1]);
+      rs[cq * 128 + m] = rr.x + rr.y;
       named_bar(1, 32 * G::SMW);
-      const float rtot = rs[m] + rs[128 + m];
+      const float rtot = (rs[m] + rs[128 + m]) + (rs[256 + m] + rs[384 + m]);
       if (gm < a.M) {
         const float sc = a.sgn[b] * (1.f / 16384.f);
         const float pi = rtot * sc;
-        const float* sh = a.shift + (size_t)b * D + half * DH;
-        const size_t row = ((size_t)b * a.M + gm) * D + half * DH;
+        const float* sh = a.shift + (size_t)b * D + cq * DQ;
+        const size_t row = ((size_t)b * a.M + gm) * D + cq * DQ;
         if (a.owner_z) {
           // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
           if (a.gz) {
 #pragma unroll
-            for (int d4 = 0; d4 < DH; d4 += 4) {
+            for (int d4 = 0; d4 < DQ; d4 += 4) {
               const float4 z4 = *reinterpret_cast<const float4*>(a.z + row + d4);
               const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
               float o[4];
@@ -981,7 +1035,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         } else {
           // G = sum P (X = [z'^2, z']): A2 = sum P z'^2, A1 = sum P z'
 #pragma unroll
-          for (int d4 = 0; d4 < DH; d4 += 4) {
+          for (int d4 = 0; d4 < DQ; d4 += 4) {
             const float4 m4 = *reinterpret_cast<const float4*>(a.mu + row + d4);
             const float4 v4 = *reinterpret_cast<const float4*>(a.lv + row + d4);
             const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -998,14 +1052,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
             if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
           }
         }
-        if (a.rowsum && half == 0) a.rowsum[(size_t)b * a.M + gm] = pi;
+        if (a.rowsum && cq == 0) a.rowsum[(size_t)b * a.M + gm] = pi;
       }
     }
-    TMC_PROF_END(warp == 2 && lane == 0, 13, _tr2);
+    TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == G::SMW + 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -1069,7 +1123,7 @@ constexpr int kDefaultGradTerms = 3;
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
-  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, shift = 0, rterm2 = 0, sgn = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, sgn = 0;
   bool bwd_ok = false;      // reverse pass on tensor cores
 };
 
@@ -1110,6 +1164,7 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     const int Cpad = (dir == TMC_DIR_DOWN) ? t.KpPad : t.KzPad;
     const int Rpad = (dir == TMC_DIR_DOWN) ? t.KzPad : t.KpPad;
     t.cb2 = tc_carve(cur, Bn * Cpad * 4);
+    t.bx = tc_carve(cur, Bn * (Cpad / 128) * tc::kBxBytes);
     t.shift = tc_carve(cur, Bn * D[i] * 4);
     t.rterm2 = tc_carve(cur, Bn * Rpad * 4);
     t.sgn = tc_carve(cur, Bn * 4);
@@ -1190,6 +1245,7 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   cbA.betaStride = t.KpPad;
   cbA.C = a.C; cbA.Cpad = Cpad;
   cbA.cb2 = reinterpret_cast<float*>(w + t.cb2);
+  cbA.bx = w + t.bx;
   cbA.cbmax = a.cbmax;
   cbA.off_cb = a.off_cb; cbA.off_rb = a.off_rb; cbA.off_out = a.off_out;
   tc::tc_colbias_kernel<<<a.B, 256, 0, s>>>(cbA);
@@ -1200,6 +1256,7 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   f.a_tiles = (zrows ? t.KzPad : t.KpPad) / 128;
   f.b_tiles = Cpad / 128;
   f.cb2 = cbA.cb2;
+  f.Bx = cbA.bx;
   f.ell_add = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
   f.ell_stride = t.KpPad;
   f.out_add = a.rb;

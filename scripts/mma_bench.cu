@@ -18,6 +18,10 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
 }
 
 template <int MODE>   // 0: SS K-major N=128; 1: SS N=64; 2: TS (A in TMEM) B MN-major N=64; 3: TS N=128; 4: SS N=256
+                      // 5: the reverse pass's tile mix (12 SS N=128 into cols 0.., 24 TS N=64 into cols 384..); n = tiles
+                      // 6: as 5 while warps 1-3 stream tcgen05.ld/st over TMEM columns 128..383 (softmax-like traffic)
+                      // 7: as 5 while warps 1-3 stream LDS.128 reads of shared memory (port contention)
+                      // 8: as 5 with the S MMAs in TS mode (A from TMEM cols 448..511)
 __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -44,6 +48,41 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
     constexpr uint32_t bmaj = (MODE >= 2 && MODE <= 3) ? 1u : 0u;
     constexpr uint32_t idesc = (1u << 4) | (bmaj << 16) | ((N >> 3) << 17) | ((128u >> 4) << 24);
     long long t0 = clock64();
+    if constexpr (MODE == 8) {
+      constexpr uint32_t idS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idG = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 12; ++k) {
+          const uint64_t b = sdesc(Bs + (k & 3) * 32);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + (i % 3) * 128),
+                       "r"(tmem + 448 + (k & 7) * 8), "l"(b), "r"(idS), "r"((uint32_t)(k != 0)));
+        }
+        for (int k = 0; k < 24; ++k) {
+          const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
+                       "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+        }
+      }
+    } else if constexpr (MODE >= 5) {
+      constexpr uint32_t idS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idG = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 12; ++k) {
+          const uint64_t a = sdesc(A + (k & 3) * 32), b = sdesc(Bs + (k & 3) * 32);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (i % 3) * 128),
+                       "l"(a), "l"(b), "r"(idS), "r"((uint32_t)(k != 0)));
+        }
+        for (int k = 0; k < 24; ++k) {
+          const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
+                       "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+        }
+      }
+    } else
     for (int i = 0; i < n; ++i) {
       const uint32_t acc = i ? 1u : 0u;
       const uint32_t koff = (i & 3) * 32;
@@ -66,6 +105,30 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
         smem_u32(&bar)));
     long long t1 = clock64();
     if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  if (MODE == 7 && warp != 0) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* p4 = reinterpret_cast<const float4*>(smem);
+    for (int i = 0; i < n * 64; ++i) {
+      const float4 q = p4[(i * 32 + (threadIdx.x & 31) + warp * 1024) & 4095];
+      acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+    }
+    if (acc.x == 1234.f) out[1023] = 1;
+  }
+  if (MODE == 6 && warp != 0) {
+    // 3 warps (lane quarters 1-3) read and write back 64 columns per "tile", like the softmax warps
+    uint32_t v[32];
+    const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128;
+    for (int i = 0; i < n * 4; ++i) {
+      const uint32_t ta = base + (uint32_t)((i & 3) * 64);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                   : "r"(ta));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                   :: "r"(ta + 32), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -94,8 +157,11 @@ int main() {
   cudaMalloc(&d, sizeof(h));
   const int n = 4096;
   printf("{\"clk_per_mma_ss_n128\": %.1f, \"clk_per_mma_ss_n64\": %.1f, \"clk_per_mma_ts_mn_n64\": %.1f, "
-         "\"clk_per_mma_ts_mn_n128\": %.1f, \"clk_per_mma_ss_n256\": %.1f, \"err\": \"%s\"}\n",
+         "\"clk_per_mma_ts_mn_n128\": %.1f, \"clk_per_mma_ss_n256\": %.1f, \"clk_per_bwd_tile_mix\": %.1f, "
+         "\"clk_per_bwd_tile_mix_with_tmem_traffic\": %.1f, \"clk_per_bwd_tile_mix_with_lds\": %.1f, "
+         "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"err\": \"%s\"}\n",
          run<0>(sms, d, h, n), run<1>(sms, d, h, n), run<2>(sms, d, h, n), run<3>(sms, d, h, n), run<4>(sms, d, h, n),
+         run<5>(sms, d, h, 256), run<6>(sms, d, h, 256), run<7>(sms, d, h, 256), run<8>(sms, d, h, 256),
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
