@@ -17,6 +17,16 @@ def sources():
         + [os.path.join(ROOT, "include", "tmc.h")]
 
 
+def build_variant(name: str, defines, verbose: bool = False) -> str:
+    """An experiment variant of the library (e.g. libtmc_spin.so with -DTMC_SPIN_WAIT)."""
+    out = os.path.join(HERE, f"libtmc_{name}.so")
+    cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + ["-o", out, SRC]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return out
+
+
 def build_instrumented(verbose: bool = False) -> str:
     """libtmc_instr.so: the same library with per-CTA barrier-wait counters (experiments only)."""
     out = os.path.join(HERE, "libtmc_instr.so")

@@ -62,6 +62,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef TMC_SPIN_WAIT
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -75,6 +76,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#else
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+#endif
 // Optional instrumentation (-DTMC_INSTRUMENT builds libtmc_instr.so only): cycles each role spends
 // waiting on each barrier, per CTA, read back with tmc_debug_counters().
 #ifdef TMC_INSTRUMENT
@@ -92,6 +108,19 @@ __device__ unsigned long long g_tmc_prof[1024][32];
 #define TMC_PROF_WAIT(cond, slot, call) call
 #define TMC_PROF_T0(var)
 #define TMC_PROF_END(cond, slot, var)
+#endif
+// reverse-pass MMA-warp probes (off with -DTMC_MMA_PROF=0 to measure the others without them)
+#ifndef TMC_MMA_PROF
+#define TMC_MMA_PROF 1
+#endif
+#if TMC_MMA_PROF
+#define TMC_PROF_WAIT_M(slot, call) TMC_PROF_WAIT(lane == 0, slot, call)
+#define TMC_PROF_T0_M(var) TMC_PROF_T0(var)
+#define TMC_PROF_END_M(slot, var) TMC_PROF_END(lane == 0, slot, var)
+#else
+#define TMC_PROF_WAIT_M(slot, call) call
+#define TMC_PROF_T0_M(var)
+#define TMC_PROF_END_M(slot, var)
 #endif
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -563,7 +592,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
       const int b = u / groups, g = u % groups;
       float mref = -INFINITY, sum = 0.f;
       for (int j = 0; j < a.b_tiles; ++j, ++t) {
-        const int as = t & 1, s = t % ST;
+        const int as = t & 1;
         TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&acc_full[as], (t >> 1) & 1));
         tc_fence_after();
         uint32_t v[64];
@@ -687,7 +716,7 @@ struct BwdArgs {
   const float* shift;          // [B][D]
   float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
   float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
-  int dbg;                     // experiment flags: 1 no S MMA, 2 no gradient MMA, 4 no softmax math
+  int dbg;                     // experiment flags: 1 no S MMA, 2 no gradient MMA, 4 no softmax math, 8 half T bytes
 };
 
 template <int D>
@@ -697,7 +726,8 @@ struct BGeo {
   static constexpr int ATOMS = Geo<D>::ATOMS;
   static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
   static constexpr int SMW = 16;                               // softmax warps (4 per TMEM lane quarter)
-  static constexpr int THREADS = 64 + 32 * SMW;
+  static constexpr int EW = 4;                                 // epilogue warps (1 per TMEM lane quarter)
+  static constexpr int THREADS = 32 * (SMW + EW + 2);
   static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 4 * 128 * 4 + 512;
 };
 
@@ -757,15 +787,18 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 template <int D, int GT>
 __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdArgs a) {
   using G = BGeo<D>;
-  constexpr int ST = G::ST;
+  constexpr int ST = G::ST, SMW = G::SMW, EW = G::EW;
+  constexpr int W_PROD = SMW + EW, W_MMA = SMW + EW + 1;     // role warps take the highest ids
   constexpr uint32_t IDESC_S = kIdescF16M128N128;
   constexpr bool PACKED = GT >= 4;
   constexpr uint32_t GN = PACKED ? 4 * D : 2 * D;            // N of the gradient MMA
   constexpr bool PLO = (GT == 3 || GT == 5);                 // P~ lo part needed
   constexpr uint32_t IDESC_G = (1u << 4) | (1u << 16) | (GN >> 3 << 17) | ((128u >> 4) << 24);
-  // S/P~ TMEM buffers (128 columns each) ahead of the gradient accumulator: three when the
-  // accumulator fits in the last 128 columns, so S(j+1) never waits for the gradient GEMM of j-1.
-  constexpr int NSB = (GN <= 128) ? 3 : 2;
+  // TMEM: NSB S/P~ buffers of 128 columns, then GB gradient accumulators of GN columns.  Three S
+  // buffers let S(j+1) run while the gradient GEMM of j-1 still reads its P~; two accumulators let
+  // the epilogue warps drain unit u while the MMAs of unit u+1 already accumulate.
+  constexpr int NSB = (3 * 128 + 2 * GN <= 512) ? 3 : 2;
+  constexpr int GB = (NSB * 128 + 2 * GN <= 512) ? 2 : 1;
   constexpr uint32_t GCOL = NSB * 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -783,9 +816,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   uint64_t* s_full = bars + 2 + 4 * ST;     // [3]  S tile ready in TMEM buffer
   uint64_t* s_empty = bars + 5 + 4 * ST;    // [3]  buffer free (its P~ consumed by the gradient GEMM)
   uint64_t* p_full = bars + 8 + 4 * ST;     // [3]  P~ written back into the buffer
-  uint64_t* g_full = bars + 11 + 4 * ST;
-  uint64_t* g_empty = bars + 12 + 4 * ST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 4 * ST);
+  uint64_t* g_full = bars + 11 + 4 * ST;    // [2]  gradient accumulator complete
+  uint64_t* g_empty = bars + 13 + 4 * ST;   // [2]  accumulator drained by the epilogue warps
+  uint64_t* r_full = bars + 15 + 4 * ST;    // [2]  row sums of the unit written to sRs
+  uint64_t* r_empty = bars + 17 + 4 * ST;   // [2]  row sums consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19 + 4 * ST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int units = a.B * a.o_tiles;
@@ -794,13 +829,16 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     mbar_init(o_empty, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
-      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], G::SMW);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMW);
     }
-    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], G::SMW); }
-    mbar_init(g_full, 1); mbar_init(g_empty, G::SMW);
+    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMW); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&g_full[s], 1); mbar_init(&g_empty[s], EW);
+      mbar_init(&r_full[s], SMW); mbar_init(&r_empty[s], EW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == G::SMW + 1) {
+  if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -809,7 +847,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == G::SMW) {
+  if (warp == W_PROD) {
     TMC_PROF_T0(_tr0);
     if (lane == 0) {   // ---------------- producer
       uint32_t t = 0, ua = 0;
@@ -822,8 +860,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
           TMC_PROF_WAIT(true, 0, mbar_wait(&t_empty[s], ph));
-          mbar_expect_tx(&t_full[s], G::TILE);
-          bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, G::TILE, &t_full[s]);
+          {
+            const uint32_t tb = (a.dbg & 8) ? G::TILE / 2 : G::TILE;   // experiment: half the bytes
+            mbar_expect_tx(&t_full[s], tb);
+            bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, tb, &t_full[s]);
+          }
           TMC_PROF_WAIT(true, 1, mbar_wait(&h_empty[s], ph));
           mbar_expect_tx(&h_full[s], 512);
           bulk_g2s(sHt + s * 128, a.ht + ((size_t)b * a.t_tiles + j) * 128, 512, &h_full[s]);
@@ -831,49 +872,52 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
-  } else if (warp == G::SMW + 1) {
+  } else if (warp == W_MMA) {
     TMC_PROF_T0(_tr1);
     {   // ---------------- MMA issuer (whole warp, one elected lane issues)
       uint32_t t = 0, ua = 0;
       const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
       auto grad = [&](uint32_t tt, bool first) {
         const uint32_t as = tt % NSB;
-        TMC_PROF_WAIT(lane == 0, 5, mbar_wait(&p_full[as], (tt / NSB) & 1));
-        if (first) TMC_PROF_WAIT(lane == 0, 7, mbar_wait(g_empty, (ua & 1) ^ 1));
+        const uint32_t gb = ua % GB;
+        TMC_PROF_WAIT_M(5, mbar_wait(&p_full[as], (tt / NSB) & 1));
+        if (first) TMC_PROF_WAIT_M(7, mbar_wait(&g_empty[gb], ((ua / GB) & 1) ^ 1));
         tc_fence_after();
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
         const uint32_t pA = tmem + as * 128;
-        TMC_PROF_T0(_tg);
+        const uint32_t gD = tmem + GCOL + gb * GN;
+        TMC_PROF_T0_M(_tg);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (a.dbg & 2) break;
+          // P~ of K-step kk: 16 tile columns held by column quarter kk/2, hi then lo (16 TMEM columns each)
           const uint32_t phi = pA + (kk >> 1) * 32 + (kk & 1) * 8, plo = phi + 16;
           const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
           const uint32_t acc0 = (!first || kk) ? 1u : 0u;
           if constexpr (PACKED) {
-            if constexpr (GT == 5) mma_f16_ts(tmem + GCOL, plo, thi, IDESC_G, acc0);
-            mma_f16_ts(tmem + GCOL, phi, thi, IDESC_G, GT == 5 ? 1u : acc0);
+            if constexpr (GT == 5) mma_f16_ts(gD, plo, thi, IDESC_G, acc0);
+            mma_f16_ts(gD, phi, thi, IDESC_G, GT == 5 ? 1u : acc0);
           } else {
-            if constexpr (GT >= 3) mma_f16_ts(tmem + GCOL, plo, thi, IDESC_G, acc0);
-            if constexpr (GT >= 2) mma_f16_ts(tmem + GCOL, phi, tlo, IDESC_G, GT >= 3 ? 1u : acc0);
-            mma_f16_ts(tmem + GCOL, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
+            if constexpr (GT >= 3) mma_f16_ts(gD, plo, thi, IDESC_G, acc0);
+            if constexpr (GT >= 2) mma_f16_ts(gD, phi, tlo, IDESC_G, GT >= 3 ? 1u : acc0);
+            mma_f16_ts(gD, phi, thi, IDESC_G, GT >= 2 ? 1u : acc0);
           }
         }
-        TMC_PROF_END(lane == 0, 11, _tg);
-        TMC_PROF_T0(_tc);
+        TMC_PROF_END_M(11, _tg);
+        TMC_PROF_T0_M(_tc);
         mma_commit(&t_empty[tt % ST]);
         mma_commit(&s_empty[as]);
-        TMC_PROF_END(lane == 0, 16, _tc);
+        TMC_PROF_END_M(16, _tc);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        TMC_PROF_WAIT(lane == 0, 6, mbar_wait(o_full, ua & 1));
+        TMC_PROF_WAIT_M(6, mbar_wait(o_full, ua & 1));
         for (int j = 0; j < a.t_tiles; ++j, ++t) {
           const int s = t % ST, as = t % NSB;
-          TMC_PROF_WAIT(lane == 0, 3, mbar_wait(&t_full[s], (t / ST) & 1));
-          TMC_PROF_WAIT(lane == 0, 4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
-          TMC_PROF_WAIT(lane == 0, 17, tc_fence_after());
+          TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
+          TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
+          TMC_PROF_WAIT_M(17, tc_fence_after());
           const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
-          TMC_PROF_T0(_ts);
+          TMC_PROF_T0_M(_ts);
 #pragma unroll
           for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
 #pragma unroll
@@ -891,27 +935,27 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
               mma_f16(d, sdesc(oBase + o), sdesc(Ts + o), IDESC_S, 1u);
             }
           }
-          TMC_PROF_END(lane == 0, 15, _ts);
-          TMC_PROF_T0(_tc2);
+          TMC_PROF_END_M(15, _ts);
+          TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
-          TMC_PROF_END(lane == 0, 18, _tc2);
+          TMC_PROF_END_M(18, _tc2);
           if (j > 0) grad(t - 1, j == 1);
         }
         grad(t - 1, a.t_tiles == 1);
-        mma_commit(g_full);
+        mma_commit(&g_full[ua % GB]);
         mma_commit(o_empty);
       }
     }
     TMC_PROF_END(lane == 0, 12, _tr1);
-  } else {
+  } else if (warp < SMW) {
     TMC_PROF_T0(_tr2);
-    // ---------------- softmax / P~ warps (16) + epilogue
+    // ---------------- softmax / P~ warps (16)
     // warp -> (TMEM lane quarter, column quarter cq): 32 columns of every S tile; P~ hi/lo go back
     // into those same 32 columns (hi in the first 16, lo in the last 16), so no warp writes TMEM
     // columns another warp still has to read.
     const int sw = warp;
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
-    const int cq = sw >> 2;                     // column quarter of the tile (and quarter of the dims)
+    const int cq = sw >> 2;                     // column quarter of the tile
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
@@ -927,8 +971,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         tc_fence_after();
         uint32_t v[32];
         const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
+        TMC_PROF_T0(_tl);
         TMC_LD32(taddr, v);
         tmem_ld_wait();
+        TMC_PROF_END(sw == 0 && lane == 0, 19, _tl);
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
         const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
         uint32_t hi[16], lo[16];
@@ -962,104 +1008,114 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
+        TMC_PROF_T0(_tst);
         TMC_ST16(taddr, hi);
         if constexpr (PLO) TMC_ST16(taddr + 16, lo);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
+        TMC_PROF_END(sw == 0 && lane == 0, 20, _tst);
       }
-      // ---------------- epilogue: G -> gradients (this warp: dims [cq*D/4, (cq+1)*D/4))
-      constexpr int DQ = D / 4;
-      TMC_PROF_WAIT(sw == 0 && lane == 0, 10, mbar_wait(g_full, ua & 1));
+      // this column quarter's row sums -> the epilogue warps
+      mbar_wait(&r_empty[ua & 1], ((ua >> 1) & 1) ^ 1);
+      const float2 rr = __fadd2_rn(racc[0], racc[1]);
+      sRs[(ua & 1) * 512 + cq * 128 + m] = rr.x + rr.y;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_full[ua & 1]);
+    }
+    TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
+  } else {
+    // ---------------- epilogue warps (4, one per TMEM lane quarter): G -> gradients, off the
+    // softmax warps' critical path (they already stream the next unit's tiles).
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint32_t ua = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      const int b = u / a.o_tiles, mt = u % a.o_tiles;
+      const int gm = mt * 128 + m;
+      const uint32_t gb = ua % GB;
+      mbar_wait(&r_full[ua & 1], (ua >> 1) & 1);
+      const float* rs = sRs + (ua & 1) * 512;
+      const float rtot = (rs[m] + rs[128 + m]) + (rs[256 + m] + rs[384 + m]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_empty[ua & 1]);
+      TMC_PROF_WAIT(warp == SMW && lane == 0, 10, mbar_wait(&g_full[gb], (ua / GB) & 1));
       tc_fence_after();
-      float g0[DQ], g1[DQ];          // G[:, d] and G[:, D + d] for this warp's dims
-      {
-        uint32_t* r0 = reinterpret_cast<uint32_t*>(g0);
-        uint32_t* r1 = reinterpret_cast<uint32_t*>(g1);
-        const uint32_t gaddr = tmem + lane_off + GCOL + cq * DQ;
-        if constexpr (DQ == 8) {
-          TMC_LD8(gaddr, r0);
-          TMC_LD8(gaddr + D, r1);
-        } else {
-          TMC_LD16(gaddr, r0);
-          TMC_LD16(gaddr + D, r1);
-        }
+      const float sc = a.sgn[b] * (1.f / 16384.f);
+      const float pi = rtot * sc;
+      const bool live = gm < a.M;
+      const float* sh = a.shift + (size_t)b * D;
+      const size_t row = ((size_t)b * a.M + (live ? gm : 0)) * D;
+      const uint32_t gaddr = tmem + lane_off + GCOL + gb * GN;
+#pragma unroll 1
+      for (int d0 = 0; d0 < D; d0 += 8) {
+        uint32_t r0[8], r1[8];
+        TMC_LD8(gaddr + d0, r0);
+        TMC_LD8(gaddr + D + d0, r1);
         if constexpr (PACKED) {     // + the T_lo column half
-          uint32_t q0[DQ], q1[DQ];
-          if constexpr (DQ == 8) {
-            TMC_LD8(gaddr + 2 * D, q0);
-            TMC_LD8(gaddr + 3 * D, q1);
-          } else {
-            TMC_LD16(gaddr + 2 * D, q0);
-            TMC_LD16(gaddr + 3 * D, q1);
-          }
+          uint32_t q0[8], q1[8];
+          TMC_LD8(gaddr + 2 * D + d0, q0);
+          TMC_LD8(gaddr + 3 * D + d0, q1);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < DQ; ++e) {
-            g0[e] += __uint_as_float(q0[e]);
-            g1[e] += __uint_as_float(q1[e]);
+          for (int e = 0; e < 8; ++e) {
+            r0[e] = __float_as_uint(__uint_as_float(r0[e]) + __uint_as_float(q0[e]));
+            r1[e] = __float_as_uint(__uint_as_float(r1[e]) + __uint_as_float(q1[e]));
           }
         }
         tmem_ld_wait();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(g_empty);
-      float* rs = sRs + (ua & 1) * 512;
-      const float2 rr = __fadd2_rn(racc[0], racc[1]);
-      rs[cq * 128 + m] = rr.x + rr.y;
-      named_bar(1, 32 * G::SMW);
-      const float rtot = (rs[m] + rs[128 + m]) + (rs[256 + m] + rs[384 + m]);
-      if (gm < a.M) {
-        const float sc = a.sgn[b] * (1.f / 16384.f);
-        const float pi = rtot * sc;
-        const float* sh = a.shift + (size_t)b * D + cq * DQ;
-        const size_t row = ((size_t)b * a.M + gm) * D + cq * DQ;
+        if (!live) continue;
+        float g0[8], g1[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { g0[e] = __uint_as_float(r0[e]); g1[e] = __uint_as_float(r1[e]); }
         if (a.owner_z) {
           // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
           if (a.gz) {
 #pragma unroll
-            for (int d4 = 0; d4 < DQ; d4 += 4) {
-              const float4 z4 = *reinterpret_cast<const float4*>(a.z + row + d4);
+            for (int d4 = 0; d4 < 8; d4 += 4) {
+              const float4 z4 = *reinterpret_cast<const float4*>(a.z + row + d0 + d4);
               const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
               float o[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float zp = zz[e] - sh[d4 + e];
+                const float zp = zz[e] - sh[d0 + d4 + e];
                 o[e] = (g1[d4 + e] + 2.f * zp * g0[d4 + e]) * (sc * kLn2);
               }
-              *reinterpret_cast<float4*>(a.gz + row + d4) = make_float4(o[0], o[1], o[2], o[3]);
+              *reinterpret_cast<float4*>(a.gz + row + d0 + d4) = make_float4(o[0], o[1], o[2], o[3]);
             }
           }
         } else {
           // G = sum P (X = [z'^2, z']): A2 = sum P z'^2, A1 = sum P z'
 #pragma unroll
-          for (int d4 = 0; d4 < DQ; d4 += 4) {
-            const float4 m4 = *reinterpret_cast<const float4*>(a.mu + row + d4);
-            const float4 v4 = *reinterpret_cast<const float4*>(a.lv + row + d4);
+          for (int d4 = 0; d4 < 8; d4 += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(a.mu + row + d0 + d4);
+            const float4 v4 = *reinterpret_cast<const float4*>(a.lv + row + d0 + d4);
             const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
             float om[4], ov[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float mp = mm[e] - sh[d4 + e];
+              const float mp = mm[e] - sh[d0 + d4 + e];
               const float lam = __expf(-vv[e]);
               const float A1 = g1[d4 + e] * sc, A2 = g0[d4 + e] * sc;
               om[e] = lam * (A1 - mp * pi);
               ov[e] = 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
             }
-            if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d4) = make_float4(om[0], om[1], om[2], om[3]);
-            if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+            if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d0 + d4) = make_float4(om[0], om[1], om[2], om[3]);
+            if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d0 + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
           }
         }
-        if (a.rowsum && cq == 0) a.rowsum[(size_t)b * a.M + gm] = pi;
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&g_empty[gb]);
+      if (live && a.rowsum) a.rowsum[(size_t)b * a.M + gm] = pi;
     }
-    TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == G::SMW + 1) {
+  if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -1343,7 +1399,7 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
   f.shift = reinterpret_cast<const float*>(w + t.shift);
   f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
   f.rowsum = own_rows ? nullptr : a.colsum;
-  f.dbg = (tc_debug_flags() >> 2) & 7;
+  f.dbg = (tc_debug_flags() >> 2) & 15;
   if (t.D == 32) tc_bwd_launch<32>(f, s);
   else tc_bwd_launch<64>(f, s);
   return n + 1;

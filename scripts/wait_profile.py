@@ -5,7 +5,7 @@ softmax warp 2 lane 0: 8 acc/S-full, 9 bias-full, 10 G-full, 13 total."""
 import ctypes, json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["TMC_LIB_PATH"] = os.path.join(ROOT, "paper_1806_08593_b200", "libtmc_instr.so")
+os.environ.setdefault("TMC_LIB_PATH", os.path.join(ROOT, "paper_1806_08593_b200", "libtmc_instr.so"))
 import numpy as np, torch
 import tmc_workload as tw
 import paper_1806_08593_b200 as tmc
@@ -33,7 +33,8 @@ counters()
 names = {0: "prod.ring_empty", 1: "prod.bias_empty", 2: "prod.own_empty", 14: "prod.total",
          3: "mma.ring_full", 4: "mma.acc_empty", 5: "mma.P_full", 6: "mma.own_full", 7: "mma.G_empty", 12: "mma.total",
          11: "mma.issue_grad", 15: "mma.issue_S", 16: "mma.commit_grad", 17: "mma.fence", 18: "mma.commit_S",
-         8: "smx.acc_full", 9: "smx.bias_full", 10: "smx.G_full", 13: "smx.total"}
+         8: "smx.acc_full", 9: "smx.bias_full", 10: "smx.G_full", 13: "smx.total",
+         19: "smx.tmem_ld", 20: "smx.tmem_st+arrive", 21: "smx.epilogue", 22: "smx.hom_load"}
 for phase in ("fwd", "bwd"):
     if phase == "fwd":
         tmc.tmc_forward(g, inp, logp, ws, None, s)
