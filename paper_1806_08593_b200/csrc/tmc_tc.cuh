@@ -1405,7 +1405,290 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
   return n + 1;
 }
 
-inline bool tc_factors_ok(int, int, int) { return false; }
-inline tmc_status tc_factors(const tmc_latent_in*, float*, int, int, int, int, cudaStream_t) { return TMC_OK; }
+// ------------------------------------------------------------------------------ K2: tmc_factors on tensor cores
+namespace tc {
+// Materialised pairwise log-factor of one latent:
+//   logf[b][a][c] = log N(z_a; mu_c, diag e^{v_c}) - logq[a] = S[a,c] + beta[c] - logq[a],
+//   S = X.Y^T (X = [z'^2, z'], Y = [-lam/2, lam mu'], z' = z - s, mu' = mu - s), 3-term fp16 split,
+//   beta[c] = -1/2 sum_d (lam mu'^2 + v + ln 2 pi)  ("norm + log-det" in the epilogue).
+// No workspace: the CTA builds its operand images in shared memory from the fp32 inputs.  Persistent;
+// unit = (datapoint, 128-row tile of z).  8 convert/epilogue warps (TMEM lane quarter x column half)
+// build the X image once per unit and the Y image + beta of every column tile (double buffered),
+// the MMA warp runs the 3-term product into double-buffered TMEM accumulators, and the same warps
+// drain S, add the norm/log-det/-logq terms and store logf rows (HBM-write bound: 4 B per pair).
+// The shift s (any s is exact algebra) is the mean of mu over the unit's first column tile.
+struct FacArgs {
+  const float *z, *mu, *lv, *logq;
+  float* logf;
+  int B, Kz, Kp;
+};
+
+template <int D>
+struct FGeo {
+  static constexpr int TILE = Geo<D>::TILE, PART = Geo<D>::PART, ATOMS = Geo<D>::ATOMS;
+  static constexpr int CW = 8;                         // convert / epilogue warps
+  static constexpr int THREADS = 32 * (CW + 1);        // + MMA warp
+  static constexpr size_t SMEM = 1024 + 3 * (size_t)TILE + 2 * 128 * 4 + 128 * 4 + 64 * 4 + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const FacArgs a) {
+  using G = FGeo<D>;
+  constexpr int CW = G::CW, W_MMA = CW;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sX = smem;                                            // X image (hi, lo)
+  uint8_t* sY = sX + G::TILE;                                    // 2 Y images
+  float* sBeta = reinterpret_cast<float*>(sY + 2 * (size_t)G::TILE);   // [2][128]
+  float* sLq = sBeta + 256;                                      // [128] logq of the unit's rows
+  float* sSh = sLq + 128;                                        // [64] shift
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSh + 64);
+  uint64_t* y_full = bars;        // [2] Y image + beta ready (CW warps)
+  uint64_t* y_empty = bars + 2;   // [2] MMA done reading it
+  uint64_t* acc_full = bars + 4;  // [2]
+  uint64_t* acc_empty = bars + 6; // [2] (CW warps)
+  uint64_t* x_full = bars + 8;    // X image ready (CW warps)
+  uint64_t* x_empty = bars + 9;   // MMA done with the unit's X image
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rtiles = (a.Kz + 127) / 128, ctiles = (a.Kp + 127) / 128;
+  const int units = a.B * rtiles;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&y_full[i], CW); mbar_init(&y_empty[i], 1);
+      mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], CW);
+    }
+    mbar_init(x_full, CW); mbar_init(x_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == W_MMA) {
+    uint32_t t = 0, ua = 0;
+    const uint32_t xBase = smem_u32(sX), yBase = smem_u32(sY);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      mbar_wait(x_full, ua & 1);
+      for (int ct = 0; ct < ctiles; ++ct, ++t) {
+        const uint32_t buf = t & 1, ph = (t >> 1) & 1;
+        mbar_wait(&y_full[buf], ph);
+        mbar_wait(&acc_empty[buf], ph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * 128, Y = yBase + buf * G::TILE;
+#pragma unroll
+        for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t o = at * kAtomBytes + kk * 32;
+            mma_f16(d, sdesc(xBase + o), sdesc(Y + G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
+            mma_f16(d, sdesc(xBase + G::PART + o), sdesc(Y + o), kIdescF16M128N128, 1u);
+          }
+        }
+#pragma unroll
+        for (int at = 0; at < G::ATOMS; ++at) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t o = at * kAtomBytes + kk * 32;
+            mma_f16(d, sdesc(xBase + o), sdesc(Y + o), kIdescF16M128N128, 1u);
+          }
+        }
+        mma_commit(&y_empty[buf]);
+        mma_commit(&acc_full[buf]);
+      }
+      mma_commit(x_empty);
+    }
+  } else {
+    // ---------------- convert / epilogue warps
+    const int quarter = warp & 3, half = warp >> 2;
+    const int m = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    constexpr int CPR = D / 4, HC = D / 8, RPI = 256 / CPR;   // 8-feature chunks per image row
+    const int j = tid % CPR, rsub = tid / CPR;
+    const int dj = (j < HC ? j : j - HC) * 8;
+    uint32_t t = 0, ua = 0;
+    auto store16 = [&](uint8_t* img, int r, const float* vals) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __half2 h = __floats2half2_rn(vals[2 * q], vals[2 * q + 1]);
+        const float2 hf = __half22float2(h);
+        __half2 l = __floats2half2_rn(vals[2 * q] - hf.x, vals[2 * q + 1] - hf.y);
+        hi[q] = *reinterpret_cast<uint32_t*>(&h);
+        lo[q] = *reinterpret_cast<uint32_t*>(&l);
+      }
+      const uint32_t off = swz_off(r, j * 8);
+      *reinterpret_cast<uint4*>(img + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(img + G::PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    };
+    auto build_y = [&](int b, int ct, uint32_t buf) {
+      const float* mub = a.mu + (size_t)b * a.Kp * D;
+      const float* lvb = a.lv + (size_t)b * a.Kp * D;
+      uint8_t* img = sY + buf * G::TILE;
+      for (int r0 = 0; r0 < 128; r0 += RPI) {
+        const int r = r0 + rsub, c = ct * 128 + r;
+        float y[8];
+        float bsum = 0.f;
+        if (c < a.Kp) {
+          const float4* lv4 = reinterpret_cast<const float4*>(lvb + (size_t)c * D + dj);
+          const float4* mu4 = reinterpret_cast<const float4*>(mub + (size_t)c * D + dj);
+          const float4 va = lv4[0], vb = lv4[1], ma = mu4[0], mb = mu4[1];
+          const float vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+          const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float lam = __expf(-vv[e]);
+            const float mp = mm[e] - sSh[dj + e];
+            if (j < HC) {
+              y[e] = -0.5f * lam;
+              bsum += lam * mp * mp + vv[e] + kLog2Pi;
+            } else {
+              y[e] = lam * mp;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) y[e] = 0.f;
+        }
+        store16(img, r, y);
+#pragma unroll
+        for (int o = CPR / 2; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+        if (j == 0) sBeta[buf * 128 + r] = -0.5f * bsum;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&y_full[buf]);
+    };
+    auto epilogue = [&](int b, int rt, int ct, uint32_t buf, uint32_t ph) {
+      mbar_wait(&acc_full[buf], ph);
+      tc_fence_after();
+      uint32_t v[64];
+      const uint32_t taddr = tmem + lane_off + buf * 128 + half * 64;
+      TMC_LD32(taddr, v);
+      TMC_LD32(taddr + 32, (v + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      const int arow = rt * 128 + m;
+      if (arow < a.Kz) {
+        const float lq = sLq[m];
+        const float* bt = sBeta + buf * 128 + half * 64;
+        const int c0 = ct * 128 + half * 64;
+        float* dst = a.logf + ((size_t)b * a.Kz + arow) * a.Kp + c0;
+        const int nc = min(64, a.Kp - c0);
+        if (nc == 64 && (a.Kp & 3) == 0) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            *reinterpret_cast<float4*>(dst + 4 * q) =
+                make_float4(__uint_as_float(v[4 * q]) + bt[4 * q] - lq, __uint_as_float(v[4 * q + 1]) + bt[4 * q + 1] - lq,
+                            __uint_as_float(v[4 * q + 2]) + bt[4 * q + 2] - lq, __uint_as_float(v[4 * q + 3]) + bt[4 * q + 3] - lq);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            if (q < nc) dst[q] = __uint_as_float(v[q]) + bt[q] - lq;
+        }
+      }
+    };
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      const int b = u / rtiles, rt = u % rtiles;
+      // all CW warps must be done with the previous unit's shift / X image / logq before rewriting
+      named_bar(1, 32 * CW);
+      // shift: mean of mu over the first column tile
+      if (tid < D) {
+        const float* mub = a.mu + (size_t)b * a.Kp * D;
+        const int n = min(128, a.Kp);
+        float acc = 0.f;
+        for (int c = 0; c < n; ++c) acc += mub[(size_t)c * D + tid];
+        sSh[tid] = acc / (float)n;
+      }
+      if (tid < 128) {
+        const int arow = rt * 128 + tid;
+        sLq[tid] = arow < a.Kz ? a.logq[(size_t)b * a.Kz + arow] : 0.f;
+      }
+      named_bar(1, 32 * CW);
+      // X image of the unit (after the MMA has finished with the previous one)
+      mbar_wait(x_empty, (ua & 1) ^ 1);
+      {
+        const float* zb = a.z + (size_t)b * a.Kz * D;
+        for (int r0 = 0; r0 < 128; r0 += RPI) {
+          const int r = r0 + rsub, arow = rt * 128 + r;
+          float x[8];
+          if (arow < a.Kz) {
+            const float4* z4 = reinterpret_cast<const float4*>(zb + (size_t)arow * D + dj);
+            const float4 za = z4[0], zc = z4[1];
+            const float zz[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float zp = zz[e] - sSh[dj + e];
+              x[e] = (j < HC) ? zp * zp : zp;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = 0.f;
+          }
+          store16(sX, r, x);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(x_full);
+      }
+      // column tiles: build Y(ct) (double buffered), then drain S(ct-1)
+      for (int ct = 0; ct < ctiles; ++ct) {
+        const uint32_t tt = t + ct, buf = tt & 1, ph = (tt >> 1) & 1;
+        mbar_wait(&y_empty[buf], ph ^ 1);
+        build_y(b, ct, buf);
+        if (ct > 0) epilogue(b, rt, ct - 1, (tt - 1) & 1, ((tt - 1) >> 1) & 1);
+      }
+      {
+        const uint32_t tt = t + ctiles - 1;
+        epilogue(b, rt, ctiles - 1, tt & 1, (tt >> 1) & 1);
+      }
+      t += ctiles;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+}  // namespace tc
+
+inline bool tc_factors_ok(int Ki, int Kp, int D) { return (D == 32 || D == 64) && Ki >= 1 && Kp >= 1; }
+
+template <int D>
+inline void tc_factors_launch(const tc::FacArgs& f, cudaStream_t s) {
+  using G = tc::FGeo<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::tc_factors_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int units = f.B * ((f.Kz + 127) / 128);
+  const int grid = units < sms ? units : sms;
+  tc::tc_factors_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
+}
+
+inline tmc_status tc_factors(const tmc_latent_in* in, float* logf, int B, int Ki, int Kp, int D, cudaStream_t s) {
+  tc::FacArgs f{};
+  f.z = in->z; f.mu = in->mu; f.lv = in->logvar; f.logq = in->logq; f.logf = logf;
+  f.B = B; f.Kz = Ki; f.Kp = Kp;
+  if (D == 32) tc_factors_launch<32>(f, s);
+  else tc_factors_launch<64>(f, s);
+  return TMC_OK;
+}
 
 }  // namespace tmc

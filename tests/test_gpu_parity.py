@@ -148,6 +148,23 @@ def test_factors_kernel_values(torch_cuda):
             np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=2e-5, atol=2e-3)
 
 
+@pytest.mark.parametrize("name,kw", [("C3", dict(B=2, K=300)), ("C4", dict(B=2, K=130)), ("C2", dict(B=1, K=257)),
+                                     ("C3", dict(B=3, K=1))])
+def test_factors_tensor_core_ragged(torch_cuda, name, kw):
+    """tmc_factors on tensor cores (D in {32, 64}): several 128-row/column tiles with ragged tails,
+    every latent (including the K_p = 1 root), element by element against the fp64 oracle."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload(name, **kw)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, precision=tmc.TMC_PREC_TC)
+    inp = upload(torch, wl)
+    for i in range(len(wl.parent)):
+        out = torch.full((wl.B, wl.K[i], wl.Kp(i)), float("nan"), device="cuda")
+        tmc.tmc_factors(g, i, inp[i], out)
+        ref = oracle.factor(wl.parent, wl.K, wl.D, i, wl.z[i], wl.mu[i], wl.logvar[i], wl.logq[i])
+        np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=2e-5, atol=2e-3, err_msg=f"latent {i}")
+
+
 def test_dlogp_weights_and_zero(torch_cuda):
     wl = tw.make_workload("C4", B=4, K=24)
     w = np.array([1.0, -0.5, 0.0, 2.5])
