@@ -187,7 +187,7 @@ void launch_pass_m(const PassArgs& a, bool dense, cudaStream_t s) {
 void launch_pass(const PassArgs& a, bool zrows, int mode, bool dense, cudaStream_t s) {
   if (a.B == 0) return;
   if (zrows && !dense && a.C == 1) {   // root of a DOWN chain: K x 1 pair matrix (prior)
-    const dim3 grid((unsigned)std::min((a.R + 7) / 8, 64), (unsigned)a.B);
+    const unsigned grid = (unsigned)(((int64_t)a.B * a.R + 255) / 256);
     if (mode == 0) simt::root_down_fwd_kernel<<<grid, 256, 0, s>>>(a);
     else if (mode == 1) simt::root_down_row_kernel<<<grid, 256, 0, s>>>(a);
     else simt::root_down_col_kernel<<<a.B, 256, 0, s>>>(a);

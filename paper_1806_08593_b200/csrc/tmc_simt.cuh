@@ -474,11 +474,14 @@ __global__ void validate_kernel(const float* x, int64_t n, int allow_neginf, int
 //   column owner (MODE 2): colsum = sum_a P[a], dmu = sum_a P (z - mu) lam, dv = 1/2 sum_a P ((z-mu)^2 lam - 1)
 // Same arithmetic as pass_kernel<true, MODE, false, *> with C = 1.
 __global__ void __launch_bounds__(256) root_down_fwd_kernel(const PassArgs a) {
-  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one thread per (datapoint, sample row): the row's D values are contiguous (float4 when D % 4 == 0)
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)a.B * a.R) return;
+  const int b = (int)(idx / a.R), r = (int)(idx % a.R);
   const int D = a.D;
-  float cb0 = a.cb[b];
+  const float cb0 = a.cb[b];
   const float cbmax = (cb0 == -INFINITY) ? 0.f : cb0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (r == 0) {
     a.cbmax[b] = cbmax;
     double off = (double)cbmax;
     if (a.off_cb) off += a.off_cb[b];
@@ -487,37 +490,56 @@ __global__ void __launch_bounds__(256) root_down_fwd_kernel(const PassArgs a) {
   }
   const float* mu = a.mu + (int64_t)b * D;
   const float* lv = a.lv + (int64_t)b * D;
-  for (int r = blockIdx.x * 8 + warp; r < a.R; r += gridDim.x * 8) {
-    const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
-    float s = 0.f;
-    for (int d = lane; d < D; d += 32) {
+  const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
+  float s = 0.f;
+  if ((D & 3) == 0) {
+    for (int d = 0; d < D; d += 4) {
+      const float4 z4 = *reinterpret_cast<const float4*>(z + d);
+      const float4 m4 = *reinterpret_cast<const float4*>(mu + d);
+      const float4 v4 = *reinterpret_cast<const float4*>(lv + d);
+      const float zz[4] = {z4.x, z4.y, z4.z, z4.w}, mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float df = zz[e] - mm[e];
+        s += df * df * __expf(-vv[e]) + vv[e] + kLog2Pi;
+      }
+    }
+  } else {
+    for (int d = 0; d < D; ++d) {
       const float df = z[d] - mu[d], v = lv[d];
       s += df * df * __expf(-v) + v + kLog2Pi;
     }
-    s = warp_sum(s);
-    if (lane == 0) {
-      const float e = (cb0 == -INFINITY) ? -INFINITY : -0.5f * s + (cb0 - cbmax);
-      a.ell[(int64_t)b * a.R + r] = e;
-      const float rb = a.rb ? a.rb[(int64_t)b * a.R + r] : 0.f;
-      a.out[(int64_t)b * a.R + r] = rb + e - a.lnC;
-    }
   }
+  const float e = (cb0 == -INFINITY) ? -INFINITY : -0.5f * s + (cb0 - cbmax);
+  a.ell[(int64_t)b * a.R + r] = e;
+  const float rb = a.rb ? a.rb[(int64_t)b * a.R + r] : 0.f;
+  a.out[(int64_t)b * a.R + r] = rb + e - a.lnC;
 }
 
 __global__ void __launch_bounds__(256) root_down_row_kernel(const PassArgs a) {
-  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)a.B * a.R) return;
+  const int b = (int)(idx / a.R), r = (int)(idx % a.R);
   const int D = a.D;
+  const float e = a.ell[(int64_t)b * a.R + r];
+  const float P = (e == -INFINITY) ? 0.f : a.w[(int64_t)b * a.R + r];
+  if (a.pair) a.pair[(int64_t)b * a.R + r] = P;
+  if (!a.gz) return;
   const float* mu = a.mu + (int64_t)b * D;
   const float* lv = a.lv + (int64_t)b * D;
-  for (int r = blockIdx.x * 8 + warp; r < a.R; r += gridDim.x * 8) {
-    const float e = a.ell[(int64_t)b * a.R + r];
-    const float P = (e == -INFINITY) ? 0.f : a.w[(int64_t)b * a.R + r];
-    if (a.pair && lane == 0) a.pair[(int64_t)b * a.R + r] = P;
-    if (a.gz) {
-      const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
-      float* gz = a.gz + ((int64_t)b * a.Kz + r) * D;
-      for (int d = lane; d < D; d += 32) gz[d] = P * (mu[d] - z[d]) * __expf(-lv[d]);
+  const float* z = a.z + ((int64_t)b * a.Kz + r) * D;
+  float* gz = a.gz + ((int64_t)b * a.Kz + r) * D;
+  if ((D & 3) == 0) {
+    for (int d = 0; d < D; d += 4) {
+      const float4 z4 = *reinterpret_cast<const float4*>(z + d);
+      const float4 m4 = *reinterpret_cast<const float4*>(mu + d);
+      const float4 v4 = *reinterpret_cast<const float4*>(lv + d);
+      *reinterpret_cast<float4*>(gz + d) =
+          make_float4(P * (m4.x - z4.x) * __expf(-v4.x), P * (m4.y - z4.y) * __expf(-v4.y),
+                      P * (m4.z - z4.z) * __expf(-v4.z), P * (m4.w - z4.w) * __expf(-v4.w));
     }
+  } else {
+    for (int d = 0; d < D; ++d) gz[d] = P * (mu[d] - z[d]) * __expf(-lv[d]);
   }
 }
 
@@ -535,13 +557,23 @@ __global__ void __launch_bounds__(256) root_down_col_kernel(const PassArgs a) {
     const int d = d0 + lane;
     float am = 0.f, av = 0.f;
     const float m = d < D ? mu[d] : 0.f, lam = d < D ? __expf(-lv[d]) : 0.f;
-    for (int r = warp; r < a.R; r += 8) {
-      const float P = (ell[r] == -INFINITY) ? 0.f : w[r];
-      if (d0 == 0) psum += P;
-      if (d < D) {
-        const float df = a.z[((int64_t)b * a.Kz + r) * D + d] - m;
-        am += P * df * lam;
-        av += P * (df * df * lam - 1.f);
+    // 4 rows in flight per warp (independent loads), fixed summation order
+    for (int r0 = warp * 4; r0 < a.R; r0 += 32) {
+      float P[4], zv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + q;
+        P[q] = (r < a.R && ell[r] != -INFINITY) ? w[r] : 0.f;
+        zv[q] = (r < a.R && d < D) ? a.z[((int64_t)b * a.Kz + r) * D + d] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (d0 == 0) psum += P[q];
+        if (d < D) {
+          const float df = zv[q] - m;
+          am += P[q] * df * lam;
+          av += P[q] * (df * df * lam - 1.f);
+        }
       }
     }
     red[0][warp][lane] = am;

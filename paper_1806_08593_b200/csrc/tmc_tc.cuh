@@ -387,6 +387,7 @@ struct ColbiasArgs {
   int C, Cpad;
   float* cb2;            // [B][Cpad] out: (cb + beta - cbmax) * log2e, -inf padded
   uint8_t* bx;           // [B][Cpad/128][kBxBytes] out: the same bias as an extra K=16 MMA operand, or NULL
+  int* live;             // [B][Cpad/128] out: 1 if any column of the 128-column tile is finite
   float* cbmax;          // [B]
   const double *off_cb, *off_rb;
   double* off_out;
@@ -395,6 +396,8 @@ struct ColbiasArgs {
 __global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[32];
+  __shared__ int s_live[64];
+  if (tid < 64) s_live[tid] = 0;
   const float* cbb = a.cb + (size_t)b * a.C;
   float m = -INFINITY;
   for (int c = tid; c < a.C; c += 256) m = fmaxf(m, cbb[c]);
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
       v *= kLog2E;
     }
     a.cb2[(size_t)b * a.Cpad + c] = v;
+    if (v > -INFINITY) s_live[c / kTileRows] = 1;
     if (a.bx) {
       // row c of the extra operand: k = 0 -> fp16 hi, k = 1 -> fp16 lo of the bias (the constant A
       // operand has ones there), so the tensor core adds the column bias to S exactly to ~2^-22.
@@ -431,6 +435,8 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
       *reinterpret_cast<uint4*>(tile + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
     }
   }
+  __syncthreads();
+  if (a.live && tid < a.Cpad / kTileRows) a.live[(size_t)b * (a.Cpad / kTileRows) + tid] = s_live[tid];
   if (tid == 0) {
     a.cbmax[b] = cmax;
     double off = (double)cmax;
@@ -716,6 +722,7 @@ struct BwdArgs {
   const float* shift;          // [B][D]
   float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
   float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
+  const int *olive, *tlive;    // [B][o_tiles], [B][t_tiles]: 0 = every P~ of the tile is exactly 0 (skipped)
   int dbg;                     // experiment flags: 1 no S MMA, 2 no gradient MMA, 4 no softmax math, 8 half T bytes
 };
 
@@ -824,6 +831,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int units = a.B * a.o_tiles;
+  // Exact sparsity: a tile whose owner rows (or streamed rows) all carry weight exactly 0 has
+  // P~ == 0 everywhere, so every role skips it consistently (phase counters count live work only).
+  auto olive = [&](int b, int mt) -> bool { return !a.olive || a.olive[(size_t)b * a.o_tiles + mt]; };
+  auto tlive = [&](int b, int j) -> bool { return !a.tlive || a.tlive[(size_t)b * a.t_tiles + j]; };
   if (tid == 0) {
     mbar_init(o_full, 1);
     mbar_init(o_empty, 1);
@@ -851,12 +862,15 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     TMC_PROF_T0(_tr0);
     if (lane == 0) {   // ---------------- producer
       uint32_t t = 0, ua = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = u / a.o_tiles, mt = u % a.o_tiles;
+        if (!olive(b, mt)) continue;
         TMC_PROF_WAIT(true, 2, mbar_wait(o_empty, (ua & 1) ^ 1));
+        ++ua;
         mbar_expect_tx(o_full, G::TILE);
         bulk_g2s(sO, a.Ot + ((size_t)b * a.o_tiles + mt) * G::TILE, G::TILE, o_full);
-        for (int j = 0; j < a.t_tiles; ++j, ++t) {
+        for (int j = 0; j < a.t_tiles; ++j) {
+          if (!tlive(b, j)) continue;
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
           TMC_PROF_WAIT(true, 0, mbar_wait(&t_empty[s], ph));
@@ -868,6 +882,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           TMC_PROF_WAIT(true, 1, mbar_wait(&h_empty[s], ph));
           mbar_expect_tx(&h_full[s], 512);
           bulk_g2s(sHt + s * 128, a.ht + ((size_t)b * a.t_tiles + j) * 128, 512, &h_full[s]);
+          ++t;
         }
       }
     }
@@ -909,9 +924,13 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         mma_commit(&s_empty[as]);
         TMC_PROF_END_M(16, _tc);
       };
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = u / a.o_tiles, mt = u % a.o_tiles;
+        if (!olive(b, mt)) continue;
         TMC_PROF_WAIT_M(6, mbar_wait(o_full, ua & 1));
-        for (int j = 0; j < a.t_tiles; ++j, ++t) {
+        int jj = 0;                      // live streamed tiles so far in this unit
+        for (int j = 0; j < a.t_tiles; ++j) {
+          if (!tlive(b, j)) continue;
           const int s = t % ST, as = t % NSB;
           TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
           TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
@@ -939,11 +958,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
           TMC_PROF_END_M(18, _tc2);
-          if (j > 0) grad(t - 1, j == 1);
+          if (jj > 0) grad(t - 1, jj == 1);
+          ++jj;
+          ++t;
         }
-        grad(t - 1, a.t_tiles == 1);
+        if (jj > 0) grad(t - 1, jj == 1);
         mma_commit(&g_full[ua % GB]);
         mma_commit(o_empty);
+        ++ua;
       }
     }
     TMC_PROF_END(lane == 0, 12, _tr1);
@@ -959,13 +981,15 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int b = u / a.o_tiles, mt = u % a.o_tiles;
+      if (!olive(b, mt)) continue;
       const int gm = mt * 128 + m;
       const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
       const float2 hom2 = make_float2(hom, hom);
       float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      for (int j = 0; j < a.t_tiles; ++j, ++t) {
+      for (int j = 0; j < a.t_tiles; ++j) {
+        if (!tlive(b, j)) continue;
         const int as = t % NSB, s = t % ST;
         TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
@@ -1016,6 +1040,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
         TMC_PROF_END(sw == 0 && lane == 0, 20, _tst);
+        ++t;
       }
       // this column quarter's row sums -> the epilogue warps
       mbar_wait(&r_empty[ua & 1], ((ua >> 1) & 1) ^ 1);
@@ -1023,6 +1048,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       sRs[(ua & 1) * 512 + cq * 128 + m] = rr.x + rr.y;
       __syncwarp();
       if (lane == 0) mbar_arrive(&r_full[ua & 1]);
+      ++ua;
     }
     TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
   } else {
@@ -1032,9 +1058,28 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     const int m = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t ua = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int b = u / a.o_tiles, mt = u % a.o_tiles;
       const int gm = mt * 128 + m;
+      if (!olive(b, mt)) {
+        // no owner row carries weight: every gradient of these rows is exactly 0
+        if (gm < a.M) {
+          const size_t row = ((size_t)b * a.M + gm) * D;
+#pragma unroll 1
+          for (int d = 0; d < D; d += 4) {
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a.owner_z) { if (a.gz) *reinterpret_cast<float4*>(a.gz + row + d) = z4; }
+            else {
+              if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d) = z4;
+              if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d) = z4;
+            }
+          }
+          if (a.rowsum) a.rowsum[(size_t)b * a.M + gm] = 0.f;
+        }
+        continue;
+      }
+      int nl = 0;
+      for (int j = 0; j < a.t_tiles; ++j) nl += tlive(b, j) ? 1 : 0;
       const uint32_t gb = ua % GB;
       mbar_wait(&r_full[ua & 1], (ua >> 1) & 1);
       const float* rs = sRs + (ua & 1) * 512;
@@ -1069,7 +1114,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         if (!live) continue;
         float g0[8], g1[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) { g0[e] = __uint_as_float(r0[e]); g1[e] = __uint_as_float(r1[e]); }
+        for (int e = 0; e < 8; ++e) {   // no live streamed tile: the accumulator was never written
+          g0[e] = nl ? __uint_as_float(r0[e]) : 0.f;
+          g1[e] = nl ? __uint_as_float(r1[e]) : 0.f;
+        }
         if (a.owner_z) {
           // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
           if (a.gz) {
@@ -1111,6 +1159,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       __syncwarp();
       if (lane == 0) mbar_arrive(&g_empty[gb]);
       if (live && a.rowsum) a.rowsum[(size_t)b * a.M + gm] = pi;
+      ++ua;
     }
   }
   tc_fence_before();
@@ -1130,13 +1179,16 @@ struct RowtermArgs {
   int betaStride, R, Rpad;
   float* rterm2;                 // [B][Rpad]
   float* sgn;                    // [B]
+  int* live;                     // [B][Rpad/128] 1 if any row of the 128-row tile carries weight
 };
 
 __global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[8];
   __shared__ int neg;
+  __shared__ int s_live[64];
   if (tid == 0) neg = 0;
+  if (tid < 64) s_live[tid] = 0;
   float wm = 0.f;
   for (int r = tid; r < a.R; r += 256) wm = fmaxf(wm, fabsf(a.w[(size_t)b * a.R + r]));
 #pragma unroll
@@ -1160,9 +1212,11 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
       }
     }
     a.rterm2[(size_t)b * a.Rpad + r] = v;
+    if (v > -INFINITY) s_live[r / kTileRows] = 1;
   }
   __syncthreads();
   if (tid == 0) a.sgn[b] = neg ? -ws : ws;
+  if (tid < a.Rpad / kTileRows) a.live[(size_t)b * (a.Rpad / kTileRows) + tid] = s_live[tid];
 }
 
 }  // namespace tc
@@ -1173,13 +1227,20 @@ inline int tc_debug_flags() {   // read per launch (experiments flip it within o
   return e ? std::atoi(e) : 0;
 }
 
+// Zero-weight tile skipping in the reverse pass is exact (the skipped P~ are exactly 0);
+// TMC_DENSE_REVERSE=1 disables it (every tile computed), for measurement.
+inline bool tc_dense_reverse() {
+  const char* e = std::getenv("TMC_DENSE_REVERSE");
+  return e && std::atoi(e) != 0;
+}
+
 // Default number of fp16 terms of the reverse pass's gradient GEMM (TMC_BWD_GRAD_TERMS overrides).
 constexpr int kDefaultGradTerms = 3;
 
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
-  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, sgn = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, sgn = 0, rlive = 0, clive = 0;
   bool bwd_ok = false;      // reverse pass on tensor cores
 };
 
@@ -1223,6 +1284,8 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     t.bx = tc_carve(cur, Bn * (Cpad / 128) * tc::kBxBytes);
     t.shift = tc_carve(cur, Bn * D[i] * 4);
     t.rterm2 = tc_carve(cur, Bn * Rpad * 4);
+    t.rlive = tc_carve(cur, Bn * (Rpad / 128) * 4);
+    t.clive = tc_carve(cur, Bn * (Cpad / 128) * 4);
     t.sgn = tc_carve(cur, Bn * 4);
     t.bwd_ok = true;
   }
@@ -1302,6 +1365,7 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   cbA.C = a.C; cbA.Cpad = Cpad;
   cbA.cb2 = reinterpret_cast<float*>(w + t.cb2);
   cbA.bx = w + t.bx;
+  cbA.live = reinterpret_cast<int*>(w + t.clive);
   cbA.cbmax = a.cbmax;
   cbA.off_cb = a.off_cb; cbA.off_rb = a.off_rb; cbA.off_out = a.off_out;
   tc::tc_colbias_kernel<<<a.B, 256, 0, s>>>(cbA);
@@ -1377,6 +1441,7 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
     r.beta = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
     r.betaStride = t.KpPad; r.R = a.R; r.Rpad = Rpad;
     r.rterm2 = rterm2; r.sgn = sgn;
+    r.live = reinterpret_cast<int*>(w + t.rlive);
     tc::tc_rowterm_kernel<<<a.B, 256, 0, s>>>(r);
     ++n;
   }
@@ -1399,6 +1464,12 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
   f.shift = reinterpret_cast<const float*>(w + t.shift);
   f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
   f.rowsum = own_rows ? nullptr : a.colsum;
+  if (!tc_dense_reverse()) {
+    const int* rl = reinterpret_cast<const int*>(w + t.rlive);
+    const int* cl = reinterpret_cast<const int*>(w + t.clive);
+    f.olive = own_rows ? rl : cl;
+    f.tlive = own_rows ? cl : rl;
+  }
   f.dbg = (tc_debug_flags() >> 2) & 15;
   if (t.D == 32) tc_bwd_launch<32>(f, s);
   else tc_bwd_launch<64>(f, s);
@@ -1428,7 +1499,7 @@ struct FGeo {
   static constexpr int TILE = Geo<D>::TILE, PART = Geo<D>::PART, ATOMS = Geo<D>::ATOMS;
   static constexpr int CW = 8;                         // convert / epilogue warps
   static constexpr int THREADS = 32 * (CW + 1);        // + MMA warp
-  static constexpr size_t SMEM = 1024 + 3 * (size_t)TILE + 2 * 128 * 4 + 128 * 4 + 64 * 4 + 256;
+  static constexpr size_t SMEM = 1024 + 3 * (size_t)TILE + 4 * 128 * 4 + 128 * 4 + 64 * 4 + 256;
 };
 
 template <int D>
@@ -1439,8 +1510,9 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;                                            // X image (hi, lo)
   uint8_t* sY = sX + G::TILE;                                    // 2 Y images
-  float* sBeta = reinterpret_cast<float*>(sY + 2 * (size_t)G::TILE);   // [2][128]
-  float* sLq = sBeta + 256;                                      // [128] logq of the unit's rows
+  // beta ring of 4: a warp can be building Y(ct) while a slower warp still reads beta of ct-3
+  float* sBeta = reinterpret_cast<float*>(sY + 2 * (size_t)G::TILE);   // [4][128]
+  float* sLq = sBeta + 512;                                      // [128] logq of the unit's rows
   float* sSh = sLq + 128;                                        // [64] shift
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSh + 64);
   uint64_t* y_full = bars;        // [2] Y image + beta ready (CW warps)
@@ -1526,7 +1598,7 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
       *reinterpret_cast<uint4*>(img + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(img + G::PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     };
-    auto build_y = [&](int b, int ct, uint32_t buf) {
+    auto build_y = [&](int b, int ct, uint32_t buf, uint32_t bb) {
       const float* mub = a.mu + (size_t)b * a.Kp * D;
       const float* lvb = a.lv + (size_t)b * a.Kp * D;
       uint8_t* img = sY + buf * G::TILE;
@@ -1558,13 +1630,13 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
         store16(img, r, y);
 #pragma unroll
         for (int o = CPR / 2; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
-        if (j == 0) sBeta[buf * 128 + r] = -0.5f * bsum;
+        if (j == 0) sBeta[bb * 128 + r] = -0.5f * bsum;
       }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&y_full[buf]);
     };
-    auto epilogue = [&](int b, int rt, int ct, uint32_t buf, uint32_t ph) {
+    auto epilogue = [&](int b, int rt, int ct, uint32_t buf, uint32_t ph, uint32_t bb) {
       mbar_wait(&acc_full[buf], ph);
       tc_fence_after();
       uint32_t v[64];
@@ -1578,7 +1650,7 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
       const int arow = rt * 128 + m;
       if (arow < a.Kz) {
         const float lq = sLq[m];
-        const float* bt = sBeta + buf * 128 + half * 64;
+        const float* bt = sBeta + bb * 128 + half * 64;
         const int c0 = ct * 128 + half * 64;
         float* dst = a.logf + ((size_t)b * a.Kz + arow) * a.Kp + c0;
         const int nc = min(64, a.Kp - c0);
@@ -1642,12 +1714,12 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
       for (int ct = 0; ct < ctiles; ++ct) {
         const uint32_t tt = t + ct, buf = tt & 1, ph = (tt >> 1) & 1;
         mbar_wait(&y_empty[buf], ph ^ 1);
-        build_y(b, ct, buf);
-        if (ct > 0) epilogue(b, rt, ct - 1, (tt - 1) & 1, ((tt - 1) >> 1) & 1);
+        build_y(b, ct, buf, tt & 3);
+        if (ct > 0) epilogue(b, rt, ct - 1, (tt - 1) & 1, ((tt - 1) >> 1) & 1, (tt - 1) & 3);
       }
       {
         const uint32_t tt = t + ctiles - 1;
-        epilogue(b, rt, ctiles - 1, tt & 1, (tt >> 1) & 1);
+        epilogue(b, rt, ctiles - 1, tt & 1, (tt >> 1) & 1, tt & 3);
       }
       t += ctiles;
     }

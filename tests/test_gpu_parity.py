@@ -165,6 +165,25 @@ def test_factors_tensor_core_ragged(torch_cuda, name, kw):
         np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=2e-5, atol=2e-3, err_msg=f"latent {i}")
 
 
+@pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=300)), ("C4", dict(B=3, K=200)), ("C3", dict(B=2))])
+def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw, monkeypatch):
+    """Skipping reverse-pass tiles whose weights are all exactly 0 gives the dense result exactly
+    (the skipped P~ are exact zeros); checked with one datapoint's dlogp = 0 as well."""
+    wl = tw.make_workload(name, **kw)
+    w = np.ones(wl.B)
+    w[-1] = 0.0
+    monkeypatch.setenv("TMC_DENSE_REVERSE", "1")
+    dense = run_gpu(torch_cuda, wl, dlogp=w)
+    monkeypatch.delenv("TMC_DENSE_REVERSE")
+    sparse = run_gpu(torch_cuda, wl, dlogp=w)
+    for k in dense:
+        if k == "logp":
+            assert np.array_equal(dense[k], sparse[k])
+        else:
+            for i, (x, y) in enumerate(zip(dense[k], sparse[k])):
+                assert np.array_equal(x, y), (k, i, np.abs(x - y).max())
+
+
 def test_dlogp_weights_and_zero(torch_cuda):
     wl = tw.make_workload("C4", B=4, K=24)
     w = np.array([1.0, -0.5, 0.0, 2.5])
