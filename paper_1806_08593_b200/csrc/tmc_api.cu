@@ -522,10 +522,10 @@ uint64_t tmc_launch_count(void) { return g_launches.load(); }
 #ifdef TMC_INSTRUMENT
 // Instrumented build only (libtmc_instr.so): copy (and optionally clear) the per-CTA wait counters.
 int tmc_debug_counters(unsigned long long* host, int n, int clear) {
-  const size_t bytes = sizeof(unsigned long long) * (size_t)std::min(n, 1024 * 32);
+  const size_t bytes = sizeof(unsigned long long) * (size_t)std::min(n, 1024 * 64);
   if (cudaMemcpyFromSymbol(host, tc::g_tmc_prof, bytes) != cudaSuccess) return -1;
   if (clear) {
-    static unsigned long long zeros[1024 * 32];
+    static unsigned long long zeros[1024 * 64];
     if (cudaMemcpyToSymbol(tc::g_tmc_prof, zeros, sizeof(zeros)) != cudaSuccess) return -1;
   }
   return 0;

@@ -94,7 +94,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Optional instrumentation (-DTMC_INSTRUMENT builds libtmc_instr.so only): cycles each role spends
 // waiting on each barrier, per CTA, read back with tmc_debug_counters().
 #ifdef TMC_INSTRUMENT
-__device__ unsigned long long g_tmc_prof[1024][32];
+__device__ unsigned long long g_tmc_prof[1024][64];
 #define TMC_PROF_WAIT(cond, slot, call)                                                   \
   do {                                                                                    \
     const long long _t0 = clock64();                                                      \
@@ -113,7 +113,12 @@ __device__ unsigned long long g_tmc_prof[1024][32];
 #ifndef TMC_MMA_PROF
 #define TMC_MMA_PROF 1
 #endif
-#if TMC_MMA_PROF
+#if TMC_MMA_PROF == 2
+// register-accumulated MMA-warp probes (no atomics in the loop; flushed once at the end)
+#define TMC_PROF_WAIT_M(slot, call) do { const long long _t0 = clock64(); call; mprof[slot - 3] += clock64() - _t0; } while (0)
+#define TMC_PROF_T0_M(var) const long long var = clock64()
+#define TMC_PROF_END_M(slot, var) mprof[slot - 3] += clock64() - var
+#elif TMC_MMA_PROF
 #define TMC_PROF_WAIT_M(slot, call) TMC_PROF_WAIT(lane == 0, slot, call)
 #define TMC_PROF_T0_M(var) TMC_PROF_T0(var)
 #define TMC_PROF_END_M(slot, var) TMC_PROF_END(lane == 0, slot, var)
@@ -137,6 +142,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// descriptor of (base + off) from the descriptor of base: the address field is (addr & 0x3FFFF) >> 4
+// and every shared-memory address here is < 2^18, so the offset adds without carry.
+__device__ __forceinline__ uint64_t dadd(uint64_t desc, uint32_t off_bytes) { return desc + (off_bytes >> 4); }
 // Instruction descriptor: kind::f16, A/B fp16 K-major, D fp32, M=128, N=128.
 constexpr uint32_t kIdescF16M128N128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -234,70 +242,86 @@ __device__ __forceinline__ void split16(float x, __half& hi, __half& lo) {
   lo = __float2half_rn(x - __half2float(hi));
 }
 
+// K1a: per-datapoint centering shift s[d]: the posterior-weighted mean of the samples the message
+// pass has already weighted (UP: softmax(h_i) over z_i; DOWN: softmax(m_pa) over mu_i), else mean_c mu.
+// Any s is exact algebra; a posterior-centred s keeps the expanded terms of the pairs that carry
+// weight small, so the fp32 tensor-core accumulator never holds large cancelling partial sums.
+template <int D>
+__global__ void __launch_bounds__(256) tc_shift_kernel(const PrepArgs p) {
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ float s_part[256];
+  __shared__ float s_ws[256];
+  __shared__ float s_w[2048 + 32];
+  const float* mub = p.mu + (size_t)b * p.Kp * D;
+  const float* zb = p.z + (size_t)b * p.Kz * D;
+  const float* vec = mub;
+  int nrow = p.Kp;
+  bool weighted = false;
+  if (p.wsrc && p.wlen <= 2048) {
+    vec = p.wz ? zb : mub;
+    nrow = p.wz ? p.Kz : p.Kp;
+    const float* wb = p.wsrc + (size_t)b * p.wlen;
+    float m = -INFINITY;
+    for (int k = tid; k < nrow; k += 256) m = fmaxf(m, wb[k]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_part[warp] = m;
+    __syncthreads();
+    if (tid == 0) {
+      float v = s_part[0];
+      for (int w = 1; w < 8; ++w) v = fmaxf(v, s_part[w]);
+      s_w[2048] = v;
+    }
+    __syncthreads();
+    const float mx = s_w[2048];
+    weighted = mx > -INFINITY;
+    if (weighted)
+      for (int k = tid; k < nrow; k += 256) s_w[k] = __expf(wb[k] - mx);
+    __syncthreads();
+  }
+  constexpr int G_ = 256 / D;
+  const int d = tid % D, g = tid / D;
+  float acc0 = 0.f, acc1 = 0.f, ws0 = 0.f, ws1 = 0.f;     // two independent chains (loads in flight)
+  if (weighted) {
+    int k = g;
+    for (; k + G_ < nrow; k += 2 * G_) {
+      const float w0 = s_w[k], w1 = s_w[k + G_];
+      acc0 += w0 * vec[(size_t)k * D + d];
+      acc1 += w1 * vec[(size_t)(k + G_) * D + d];
+      ws0 += w0; ws1 += w1;
+    }
+    if (k < nrow) { acc0 += s_w[k] * vec[(size_t)k * D + d]; ws0 += s_w[k]; }
+  } else {
+    for (int c = g; c < p.Kp; c += G_) acc0 += mub[(size_t)c * D + d];
+  }
+  s_part[tid] = acc0 + acc1;
+  s_ws[tid] = ws0 + ws1;
+  __syncthreads();
+  if (tid < D) {
+    float t = 0.f, ws = 0.f;
+    for (int j = 0; j < G_; ++j) { t += s_part[j * D + tid]; ws += s_ws[j * D]; }
+    if (!weighted) ws = (float)p.Kp;
+    p.shift[(size_t)b * D + tid] = t / ws;
+  }
+}
+
+// K1b: operand tile images of rows [blockIdx.y * 256, +256) of both sides (Y rows then X rows
+// share the grid: y < KpPad/256 -> param rows, else z rows).
 template <int D>
 __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
   using G = Geo<D>;
   const int b = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ float s_part[256];
+  const int tid = threadIdx.x;
   __shared__ float s_shift[D];
+  if (tid < D) s_shift[tid] = p.shift[(size_t)b * D + tid];
+  __syncthreads();
   const float* mub = p.mu + (size_t)b * p.Kp * D;
   const float* lvb = p.lv + (size_t)b * p.Kp * D;
   const float* zb = p.z + (size_t)b * p.Kz * D;
-  // centering shift s[d]: the posterior-weighted mean of the samples the message pass has
-  // already weighted (UP: softmax(h_i) over z_i; DOWN: softmax(m_pa) over mu_i), else mean_c mu.
-  // Any s is exact algebra; a posterior-centred s keeps the expanded terms of the pairs that carry
-  // weight small, so the fp32 tensor-core accumulator never holds large cancelling partial sums.
-  {
-    __shared__ float s_w[2048 + 32];
-    const float* vec = mub;
-    int nrow = p.Kp;
-    bool weighted = false;
-    if (p.wsrc && p.wlen <= 2048) {
-      vec = p.wz ? zb : mub;
-      nrow = p.wz ? p.Kz : p.Kp;
-      const float* wb = p.wsrc + (size_t)b * p.wlen;
-      float m = -INFINITY;
-      for (int k = tid; k < nrow; k += 256) m = fmaxf(m, wb[k]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) s_part[warp] = m;
-      __syncthreads();
-      if (tid == 0) {
-        float v = s_part[0];
-        for (int w = 1; w < 8; ++w) v = fmaxf(v, s_part[w]);
-        s_w[2048] = v;
-      }
-      __syncthreads();
-      const float mx = s_w[2048];
-      weighted = mx > -INFINITY;
-      if (weighted)
-        for (int k = tid; k < nrow; k += 256) s_w[k] = __expf(wb[k] - mx);
-      __syncthreads();
-    }
-    constexpr int G_ = 256 / D;
-    const int d = tid % D, g = tid / D;
-    float acc = 0.f, wsum = 0.f;
-    if (weighted) {
-      for (int k = g; k < nrow; k += G_) { acc += s_w[k] * vec[(size_t)k * D + d]; wsum += s_w[k]; }
-    } else {
-      for (int c = g; c < p.Kp; c += G_) acc += mub[(size_t)c * D + d];
-      wsum = 0.f;
-    }
-    __syncthreads();
-    s_part[tid] = acc;
-    __shared__ float s_ws[256];
-    s_ws[tid] = wsum;
-    __syncthreads();
-    if (tid < D) {
-      float t = 0.f, ws = 0.f;
-      for (int j = 0; j < G_; ++j) { t += s_part[j * D + tid]; ws += s_ws[j * D]; }
-      if (!weighted) ws = (float)p.Kp;
-      s_shift[tid] = t / ws;
-      p.shift[(size_t)b * D + tid] = t / ws;
-    }
-    __syncthreads();
-  }
+  const int ychunks = p.KpPad / 256;
+  const bool yside = (int)blockIdx.y < ychunks;
+  const int rbase = (yside ? (int)blockIdx.y : (int)blockIdx.y - ychunks) * 256;
   // Tile images: one thread per (row, 8-feature chunk) writes 16 B of the hi part and 16 B of the lo
   // part (8 consecutive chunk-threads fill one 128-byte swizzled row of an atom: coalesced).
   constexpr int CPR = D / 4;           // 8-feature chunks per row (2D features)
@@ -327,7 +351,8 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
     *reinterpret_cast<uint4*>(tile + G::PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   };
   // param rows -> Y tile image, beta
-  for (int c0 = 0; c0 < p.KpPad; c0 += RPI) {
+  if (yside)
+  for (int c0 = rbase; c0 < rbase + 256; c0 += RPI) {
     const int c = c0 + rsub;
     float y[8];
     float bsum = 0.f;
@@ -359,7 +384,8 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
     if (j == 0 && c < p.KpPad) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * bsum : 0.f;
   }
   // z rows -> X tile image
-  for (int a0 = 0; a0 < p.KzPad; a0 += RPI) {
+  if (!yside)
+  for (int a0 = rbase; a0 < rbase + 256; a0 += RPI) {
     const int a = a0 + rsub;
     float x[8];
     if (a < p.Kz) {
@@ -553,7 +579,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
           for (int rb = 0; rb < RB; ++rb) {
             if (a.dbg & 1) break;
             const uint32_t d = tmem + (uint32_t)((rb * 2 + as) * 128);
-            const uint32_t A = aBase + rb * G::TILE, Bs = bBase + s * G::TILE;
+            const uint64_t dA = sdesc(aBase + rb * G::TILE), dB = sdesc(bBase + s * G::TILE);
             // small cross terms first, the large hi*hi products last: fewer fp32 accumulator
             // roundings at large partial-sum magnitude
 #pragma unroll
@@ -561,8 +587,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t o = at * kAtomBytes + kk * 32;
-                mma_f16(d, sdesc(A + o), sdesc(Bs + G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
-                mma_f16(d, sdesc(A + G::PART + o), sdesc(Bs + o), kIdescF16M128N128, 1u);
+                mma_f16(d, dadd(dA, o), dadd(dB, G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
+                mma_f16(d, dadd(dA, G::PART + o), dadd(dB, o), kIdescF16M128N128, 1u);
               }
             }
 #pragma unroll
@@ -570,7 +596,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t o = at * kAtomBytes + kk * 32;
-                mma_f16(d, sdesc(A + o), sdesc(Bs + o), kIdescF16M128N128, 1u);
+                mma_f16(d, dadd(dA, o), dadd(dB, o), kIdescF16M128N128, 1u);
               }
             }
             // + column bias: ones(128 x 16) . [cb_hi, cb_lo, 0..]^T
@@ -890,6 +916,9 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   } else if (warp == W_MMA) {
     TMC_PROF_T0(_tr1);
     {   // ---------------- MMA issuer (whole warp, one elected lane issues)
+#if defined(TMC_INSTRUMENT) && TMC_MMA_PROF == 2
+      long long mprof[16] = {0};
+#endif
       uint32_t t = 0, ua = 0;
       const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
       auto grad = [&](uint32_t tt, bool first) {
@@ -901,13 +930,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         const uint32_t Ts = tBase + (tt % ST) * G::TILE;
         const uint32_t pA = tmem + as * 128;
         const uint32_t gD = tmem + GCOL + gb * GN;
+        const uint64_t dT = sdesc_mn(Ts, kAtomBytes);
         TMC_PROF_T0_M(_tg);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (a.dbg & 2) break;
           // P~ of K-step kk: 16 tile columns held by column quarter kk/2, hi then lo (16 TMEM columns each)
           const uint32_t phi = pA + (kk >> 1) * 32 + (kk & 1) * 8, plo = phi + 16;
-          const uint64_t thi = sdesc_mn(Ts + kk * 2048, kAtomBytes), tlo = sdesc_mn(Ts + G::PART + kk * 2048, kAtomBytes);
+          const uint64_t thi = dadd(dT, kk * 2048), tlo = dadd(dT, G::PART + kk * 2048);
           const uint32_t acc0 = (!first || kk) ? 1u : 0u;
           if constexpr (PACKED) {
             if constexpr (GT == 5) mma_f16_ts(gD, plo, thi, IDESC_G, acc0);
@@ -935,15 +965,16 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
           TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
           TMC_PROF_WAIT_M(17, tc_fence_after());
-          const uint32_t d = tmem + (uint32_t)(as * 128), Ts = tBase + s * G::TILE;
+          const uint32_t d = tmem + (uint32_t)(as * 128);
+          const uint64_t dO = sdesc(oBase), dS = sdesc(tBase + s * G::TILE);
           TMC_PROF_T0_M(_ts);
 #pragma unroll
           for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
-              mma_f16(d, sdesc(oBase + o), sdesc(Ts + G::PART + o), IDESC_S, (at | kk) ? 1u : 0u);
-              mma_f16(d, sdesc(oBase + G::PART + o), sdesc(Ts + o), IDESC_S, 1u);
+              mma_f16(d, dadd(dO, o), dadd(dS, G::PART + o), IDESC_S, (at | kk) ? 1u : 0u);
+              mma_f16(d, dadd(dO, G::PART + o), dadd(dS, o), IDESC_S, 1u);
             }
           }
 #pragma unroll
@@ -951,7 +982,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
-              mma_f16(d, sdesc(oBase + o), sdesc(Ts + o), IDESC_S, 1u);
+              mma_f16(d, dadd(dO, o), dadd(dS, o), IDESC_S, 1u);
             }
           }
           TMC_PROF_END_M(15, _ts);
@@ -967,6 +998,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         mma_commit(o_empty);
         ++ua;
       }
+#if defined(TMC_INSTRUMENT) && TMC_MMA_PROF == 2
+      if (lane == 0)
+        for (int q = 0; q < 16; ++q) atomicAdd(&g_tmc_prof[blockIdx.x & 1023][3 + q], (unsigned long long)mprof[q]);
+#endif
     }
     TMC_PROF_END(lane == 0, 12, _tr1);
   } else if (warp < SMW) {
@@ -991,7 +1026,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       for (int j = 0; j < a.t_tiles; ++j) {
         if (!tlive(b, j)) continue;
         const int as = t % NSB, s = t % ST;
-        TMC_PROF_WAIT(sw == 0 && lane == 0, 8, mbar_wait(&s_full[as], (t / NSB) & 1));
+        TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
         uint32_t v[32];
         const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
@@ -1050,7 +1085,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
       if (lane == 0) mbar_arrive(&r_full[ua & 1]);
       ++ua;
     }
-    TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
+    TMC_PROF_END(lane == 0, 48 + sw, _tr2);
   } else {
     // ---------------- epilogue warps (4, one per TMEM lane quarter): G -> gradients, off the
     // softmax warps' critical path (they already stream the next unit's tiles).
@@ -1295,7 +1330,8 @@ inline bool tc_edge_ok(const TcLatentBuf& b) { return b.ok; }
 
 template <int D>
 inline void tc_prep_launch(const tc::PrepArgs& p, int B, cudaStream_t s) {
-  tc::tc_prep_kernel<D><<<B, 256, 0, s>>>(p);
+  tc::tc_shift_kernel<D><<<B, 256, 0, s>>>(p);
+  tc::tc_prep_kernel<D><<<dim3(B, p.KpPad / 256 + p.KzPad / 256), 256, 0, s>>>(p);
 }
 
 // Operand prep of one tensor-core edge (latent i): X/Y tile images, beta and the centering shift.
@@ -1313,7 +1349,7 @@ inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in,
   p.wsrc = wsrc; p.wlen = wlen; p.wz = wz;
   if (Di == 32) tc_prep_launch<32>(p, B, s);
   else tc_prep_launch<64>(p, B, s);
-  return 1;
+  return 2;   // shift + image kernels
 }
 
 // Forward softmax variant (TMC_FWD_VARIANT overrides):
@@ -1552,14 +1588,15 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
         mbar_wait(&y_full[buf], ph);
         mbar_wait(&acc_empty[buf], ph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + buf * 128, Y = yBase + buf * G::TILE;
+        const uint32_t d = tmem + buf * 128;
+        const uint64_t dX = sdesc(xBase), dY = sdesc(yBase + buf * G::TILE);
 #pragma unroll
         for (int at = 0; at < G::ATOMS; ++at) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t o = at * kAtomBytes + kk * 32;
-            mma_f16(d, sdesc(xBase + o), sdesc(Y + G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
-            mma_f16(d, sdesc(xBase + G::PART + o), sdesc(Y + o), kIdescF16M128N128, 1u);
+            mma_f16(d, dadd(dX, o), dadd(dY, G::PART + o), kIdescF16M128N128, (at | kk) ? 1u : 0u);
+            mma_f16(d, dadd(dX, G::PART + o), dadd(dY, o), kIdescF16M128N128, 1u);
           }
         }
 #pragma unroll
@@ -1567,7 +1604,7 @@ __global__ void __launch_bounds__(FGeo<D>::THREADS, 1) tc_factors_kernel(const F
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t o = at * kAtomBytes + kk * 32;
-            mma_f16(d, sdesc(xBase + o), sdesc(Y + o), kIdescF16M128N128, 1u);
+            mma_f16(d, dadd(dX, o), dadd(dY, o), kIdescF16M128N128, 1u);
           }
         }
         mma_commit(&y_empty[buf]);

@@ -22,14 +22,18 @@ template <int MODE>   // 0: SS K-major N=128; 1: SS N=64; 2: TS (A in TMEM) B MN
                       // 6: as 5 while warps 1-3 stream tcgen05.ld/st over TMEM columns 128..383 (softmax-like traffic)
                       // 7: as 5 while warps 1-3 stream LDS.128 reads of shared memory (port contention)
                       // 8: as 5 with the S MMAs in TS mode (A from TMEM cols 448..511)
-__global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) {
+                      // 9: as 5 while 20 other warps (5 per SMSP) run an ex2/FADD2 loop (softmax-like issue load)
+                      // 10: as 5 with a tcgen05.commit after the S MMAs and two after the gradient MMAs (per tile)
+__global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
+  __shared__ uint64_t dbar[4];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
   if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&dbar[q])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
                        "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
         }
       }
-    } else if constexpr (MODE >= 5) {
+    } else if constexpr (MODE >= 5 && MODE != 9 || MODE == 9) {
       constexpr uint32_t idS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
       constexpr uint32_t idG = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
       for (int i = 0; i < n; ++i) {
@@ -75,11 +79,20 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (i % 3) * 128),
                        "l"(a), "l"(b), "r"(idS), "r"((uint32_t)(k != 0)));
         }
+        if (MODE == 10)
+          asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(&dbar[0])) : "memory");
         for (int k = 0; k < 24; ++k) {
           const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
           asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
                        "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+        }
+        if (MODE == 10) {
+          asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(&dbar[1])) : "memory");
+          asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(&dbar[2])) : "memory");
         }
       }
     } else
@@ -105,6 +118,18 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
         smem_u32(&bar)));
     long long t1 = clock64();
     if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  if (MODE == 9 && warp != 0) {
+    float2 acc = make_float2(0.f, 0.f), x = make_float2(threadIdx.x * 1e-9f, 1e-9f);
+    for (int i = 0; i < n * 96; ++i) {
+      const float2 y = __fadd2_rn(x, make_float2(-1e-3f, -2e-3f));
+      float e0, e1;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(y.x));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(y.y));
+      acc = __fadd2_rn(acc, make_float2(e0, e1));
+      x = __fadd2_rn(x, make_float2(1e-7f, 1e-7f));
+    }
+    if (acc.x == 1234.f) out[1023] = 1;
   }
   if (MODE == 7 && warp != 0) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -141,8 +166,9 @@ __global__ void __launch_bounds__(128, 1) bench(int n, unsigned long long* out) 
 template <int MODE>
 double run(int sms, unsigned long long* d, unsigned long long* h, int n) {
   cudaFuncSetAttribute(bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
-  bench<MODE><<<sms, 128, 70 * 1024>>>(n, d);
-  bench<MODE><<<sms, 128, 70 * 1024>>>(n, d);
+  const int threads = MODE == 9 ? 704 : 128;
+  bench<MODE><<<sms, threads, 70 * 1024>>>(n, d);
+  bench<MODE><<<sms, threads, 70 * 1024>>>(n, d);
   cudaDeviceSynchronize();
   cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
   double s = 0;
@@ -159,9 +185,9 @@ int main() {
   printf("{\"clk_per_mma_ss_n128\": %.1f, \"clk_per_mma_ss_n64\": %.1f, \"clk_per_mma_ts_mn_n64\": %.1f, "
          "\"clk_per_mma_ts_mn_n128\": %.1f, \"clk_per_mma_ss_n256\": %.1f, \"clk_per_bwd_tile_mix\": %.1f, "
          "\"clk_per_bwd_tile_mix_with_tmem_traffic\": %.1f, \"clk_per_bwd_tile_mix_with_lds\": %.1f, "
-         "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"err\": \"%s\"}\n",
+         "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"clk_per_bwd_tile_mix_busy_smsp\": %.1f, \"clk_per_bwd_tile_mix_3_commits\": %.1f, \"err\": \"%s\"}\n",
          run<0>(sms, d, h, n), run<1>(sms, d, h, n), run<2>(sms, d, h, n), run<3>(sms, d, h, n), run<4>(sms, d, h, n),
-         run<5>(sms, d, h, 256), run<6>(sms, d, h, 256), run<7>(sms, d, h, 256), run<8>(sms, d, h, 256),
+         run<5>(sms, d, h, 256), run<6>(sms, d, h, 256), run<7>(sms, d, h, 256), run<8>(sms, d, h, 256), run<9>(sms, d, h, 256), run<10>(sms, d, h, 256),
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
