@@ -1031,8 +1031,13 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         uint32_t v[32];
         const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
         TMC_PROF_T0(_tl);
-        TMC_LD32(taddr, v);
-        tmem_ld_wait();
+        if (!(a.dbg & 16)) {     // experiment flag 16: no TMEM traffic from the softmax warps
+          TMC_LD32(taddr, v);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = 0u;
+        }
         TMC_PROF_END(sw == 0 && lane == 0, 19, _tl);
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
         const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
@@ -1068,9 +1073,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
         TMC_PROF_T0(_tst);
-        TMC_ST16(taddr, hi);
-        if constexpr (PLO) TMC_ST16(taddr + 16, lo);
-        tmem_st_wait();
+        if (!(a.dbg & 16)) {
+          TMC_ST16(taddr, hi);
+          if constexpr (PLO) TMC_ST16(taddr + 16, lo);
+          tmem_st_wait();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
@@ -1506,7 +1513,7 @@ inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, b
     f.olive = own_rows ? rl : cl;
     f.tlive = own_rows ? cl : rl;
   }
-  f.dbg = (tc_debug_flags() >> 2) & 15;
+  f.dbg = (tc_debug_flags() >> 2) & 31;
   if (t.D == 32) tc_bwd_launch<32>(f, s);
   else tc_bwd_launch<64>(f, s);
   return n + 1;
