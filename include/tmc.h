@@ -89,6 +89,12 @@ typedef struct {
   int32_t direction;      /* tmc_direction                                                    */
   int32_t precision;      /* tmc_precision                                                    */
   uint32_t flags;         /* TMC_FLAG_*                                                       */
+  float factor_power;     /* alpha: every log-factor and observation term is multiplied by    */
+                          /* alpha, i.e. logp = log((1/prod K_i) sum prod f^alpha obs^alpha);  */
+                          /* 0 or 1 = the TMC estimate; 2 = the sum of squared importance      */
+                          /* weights of the DReGs surrogate ("running TMC again, with squared  */
+                          /* weights").  Gradients are of that logp.  tmc_factors   */
+                          /* ignores it (it materialises logf itself).                          */
 } tmc_graph;
 
 /* Per-latent inputs (DEVICE).  K_p = K[parent[i]], or 1 for a root (its prior).             */

@@ -52,7 +52,7 @@ def _load():
         _lib.or_logmmexp.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, P]
         _lib.or_factor.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P]
         _lib.or_estimate.argtypes = ([ctypes.c_int, ctypes.c_int, P, P, P] + [P] * 6 +
-                                     [ctypes.c_int, P, P] + [P] * 6 + [ctypes.c_int])
+                                     [ctypes.c_int, P, P] + [P] * 6 + [ctypes.c_int, ctypes.c_double])
     return _lib
 
 
@@ -102,11 +102,14 @@ def factor(parent, K, D, i, z, mu, logvar, logq) -> np.ndarray:
 
 
 def estimate(parent, K, D, z, mu, logvar, logq, logobs, *, logf_dense=None, direction="up",
-             dlogp=None, grads=True, pair=False, threads: Optional[int] = None) -> Dict[str, object]:
+             dlogp=None, grads=True, pair=False, threads: Optional[int] = None,
+             alpha: float = 1.0) -> Dict[str, object]:
     """Run the oracle.  Inputs are per-latent lists of float32 arrays (tmc_workload layout).
 
     Returns {"logp": float64[B], and if grads: "dz","dmu","dlogvar","dlogq","dlogobs" lists of
     float64 arrays, and if pair: "pair" list of float64[B][K_i][K_p]}.
+    alpha: factor power (every log-factor and observation term times alpha; alpha = 2 gives the
+    squared-weight estimate log((1/prod K) sum w^2) of the DReGs surrogate).
     """
     p, k, d = _graph(parent, K, D)
     n = len(p)
@@ -145,7 +148,7 @@ def estimate(parent, K, D, z, mu, logvar, logq, logobs, *, logf_dense=None, dire
         n, B, _ptr(p), _ptr(k), _ptr(d),
         arr(z), arr(mu), arr(logvar), arr(logq), arr(logobs), arr(logf_dense),
         dirc, _ptr(dl), _ptr(logp),
-        arr(pr), arr(gz), arr(gmu), arr(gv), arr(gq), arr(go), int(nt))
+        arr(pr), arr(gz), arr(gmu), arr(gv), arr(gq), arr(go), int(nt), float(alpha))
     if rc != 0:
         raise ValueError(f"or_estimate failed: {rc}")
     return out

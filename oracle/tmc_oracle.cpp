@@ -60,6 +60,9 @@ struct Graph {
 
 struct Inputs {
   const float *const *z, *const *mu, *const *logvar, *const *logq, *const *logobs, *const *logf_dense;
+  // factor power: every log-factor and observation term times alpha.  alpha = 2 is "running TMC
+  // again, with squared weights", the sum of squared weights the DReGs surrogate needs.
+  double alpha = 1.0;
 };
 
 struct Outputs {
@@ -109,12 +112,15 @@ double obs(const Inputs& in, const Graph& g, int i, int b, int a) {
 void run_datapoint(const Graph& g, const Inputs& in, const Outputs& out, int direction, int b) {
   const int n = g.n;
   std::vector<std::vector<double>> f(n), h(n), msg(n);
-  for (int i = 0; i < n; ++i) f[i] = factor(g, in, i, b);
+  for (int i = 0; i < n; ++i) {
+    f[i] = factor(g, in, i, b);
+    for (double& v : f[i]) v *= in.alpha;
+  }
 
   // O3: upward elimination, reverse topological order (parent[i] < i).
   for (int i = 0; i < n; ++i) {
     h[i].assign(g.K[i], 0.0);
-    for (int a = 0; a < g.K[i]; ++a) h[i][a] = obs(in, g, i, b, a);
+    for (int a = 0; a < g.K[i]; ++a) h[i][a] = in.alpha * obs(in, g, i, b, a);
   }
   double L_up = 0.0;
   for (int i = n - 1; i >= 0; --i) {
@@ -142,7 +148,7 @@ void run_datapoint(const Graph& g, const Inputs& in, const Outputs& out, int dir
       for (int a = 0; a < Ki; ++a) {
         std::vector<double> t(Kp);
         for (int c = 0; c < Kp; ++c) t[c] = f[i][(size_t)a * Kp + c] + (i == 0 ? 0.0 : m[c]);
-        mi[a] = obs(in, g, i, b, a) + lse(t) - (i == 0 ? 0.0 : std::log((double)Kp));
+        mi[a] = in.alpha * obs(in, g, i, b, a) + lse(t) - (i == 0 ? 0.0 : std::log((double)Kp));
       }
       m.swap(mi);
     }
@@ -173,20 +179,22 @@ void run_datapoint(const Graph& g, const Inputs& in, const Outputs& out, int dir
   // then d logN / d{z, mu, v} in the direct form.
   for (int i = 0; i < n; ++i) {
     const int Ki = g.K[i], Kp = g.Kp(i), D = g.D[i];
+    // with factor power alpha every input enters as alpha * (its log-term): chain rule factor alpha
+    const double al = in.alpha;
     if (out.pair && out.pair[i])
-      std::memcpy(out.pair[i] + (size_t)b * Ki * Kp, P[i].data(), sizeof(double) * Ki * Kp);
+      for (size_t j = 0; j < P[i].size(); ++j) out.pair[i][(size_t)b * Ki * Kp + j] = al * P[i][j];
     if (out.dlogobs && out.dlogobs[i])
-      for (int a = 0; a < Ki; ++a) out.dlogobs[i][(size_t)b * Ki + a] = pi[i][a];
+      for (int a = 0; a < Ki; ++a) out.dlogobs[i][(size_t)b * Ki + a] = al * pi[i][a];
     if (in.logf_dense) continue;
     if (out.dlogq && out.dlogq[i])
-      for (int a = 0; a < Ki; ++a) out.dlogq[i][(size_t)b * Ki + a] = -pi[i][a];
+      for (int a = 0; a < Ki; ++a) out.dlogq[i][(size_t)b * Ki + a] = -al * pi[i][a];
     const float* z = in.z[i] + (size_t)b * Ki * D;
     const float* mu = in.mu[i] + (size_t)b * Kp * D;
     const float* v = in.logvar[i] + (size_t)b * Kp * D;
     std::vector<double> dz((size_t)Ki * D, 0.0), dmu((size_t)Kp * D, 0.0), dv((size_t)Kp * D, 0.0);
     for (int a = 0; a < Ki; ++a)
       for (int r = 0; r < Kp; ++r) {
-        double p = P[i][(size_t)a * Kp + r];
+        double p = al * P[i][(size_t)a * Kp + r];
         if (p == 0.0) continue;
         for (int d = 0; d < D; ++d) {
           double zz = z[(size_t)a * D + d], mm = mu[(size_t)r * D + d], vv = v[(size_t)r * D + d];
@@ -262,11 +270,11 @@ int or_estimate(int n, int B, const int* parent, const int* K, const int* D,
                 const float* const* logq, const float* const* logobs, const float* const* logf_dense,
                 int direction, const double* dlogp, double* logp,
                 double* const* pair, double* const* dz, double* const* dmu, double* const* dlogvar,
-                double* const* dlogq, double* const* dlogobs, int nthreads) {
+                double* const* dlogq, double* const* dlogobs, int nthreads, double alpha) {
   if (!valid_graph(n, B, parent, K, D) || !logp) return -1;
   if (direction == 1 && !is_chain(n, parent)) return -2;
   Graph g{n, B, parent, K, D};
-  Inputs in{z, mu, logvar, logq, logobs, logf_dense};
+  Inputs in{z, mu, logvar, logq, logobs, logf_dense, alpha};
   Outputs out{logp, pair, dz, dmu, dlogvar, dlogq, dlogobs, dlogp};
   if (nthreads <= 1 || B <= 1) {
     for (int b = 0; b < B; ++b) run_datapoint(g, in, out, direction, b);

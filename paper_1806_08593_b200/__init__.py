@@ -37,7 +37,7 @@ class tmc_graph(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("B", ctypes.c_int32),
                 ("parent", ctypes.POINTER(ctypes.c_int32)), ("K", ctypes.POINTER(ctypes.c_int32)),
                 ("D", ctypes.POINTER(ctypes.c_int32)), ("direction", ctypes.c_int32),
-                ("precision", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("precision", ctypes.c_int32), ("flags", ctypes.c_uint32), ("factor_power", ctypes.c_float)]
 
 
 class tmc_latent_in(ctypes.Structure):
@@ -92,12 +92,13 @@ class Graph:
     direction: int = TMC_DIR_AUTO
     precision: int = TMC_PREC_AUTO
     flags: int = 0
+    factor_power: float = 1.0     # alpha: 2 gives log((1/prod K) sum w^2) (DReGs)
 
     def __post_init__(self):
         n = len(self.parent)
         self._arrs = [(ctypes.c_int32 * n)(*[int(v) for v in a]) for a in (self.parent, self.K, self.D)]
         self._c = tmc_graph(n, int(self.B), self._arrs[0], self._arrs[1], self._arrs[2],
-                            int(self.direction), int(self.precision), int(self.flags))
+                            int(self.direction), int(self.precision), int(self.flags), float(self.factor_power))
 
     @property
     def n(self) -> int:

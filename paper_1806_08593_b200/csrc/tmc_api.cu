@@ -36,6 +36,7 @@ struct EdgeBuf {
 
 struct Plan {
   int n = 0, B = 0, dir = 0, prec = 0;
+  float alpha = 1.f;
   bool dense = false;
   std::vector<int> parent, K, D, Kp;
   std::vector<std::vector<int>> children;
@@ -68,6 +69,9 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   if (g->precision < 0 || g->precision > 2) return fail(TMC_ERR_INVALID_ARG, "bad precision");
   p.n = g->n;
   p.B = g->B;
+  if (!(g->factor_power >= 0.f) || g->factor_power > 64.f)
+    return fail(TMC_ERR_INVALID_ARG, "factor_power must be in [0, 64] (0 = 1)");
+  p.alpha = g->factor_power == 0.f ? 1.f : g->factor_power;
   p.dense = dense;
   p.parent.assign(g->parent, g->parent + g->n);
   p.K.assign(g->K, g->K + g->n);
@@ -211,6 +215,7 @@ PassArgs edge_args(const Plan& p, int i, const tmc_latent_in* in, const float* c
   const EdgeBuf& e = p.e[i];
   a.B = p.B; a.R = e.R; a.C = e.C; a.D = p.D[i];
   a.Kz = p.K[i]; a.Kp = p.Kp[i];
+  a.alpha = p.alpha;
   if (dense) a.logf = dense[i];
   else { a.z = in[i].z; a.mu = in[i].mu; a.lv = in[i].logvar; }
   a.cbmax = at<float>(ws, e.cbmax);
@@ -286,6 +291,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
   for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
     UnaryBatch ub{};
     ub.B = p.B;
+    ub.alpha = p.alpha;
     ub.count = std::min(kMaxUnaryPerLaunch, p.n - i0);
     for (int j = 0; j < ub.count; ++j) {
       int i = i0 + j;
@@ -305,7 +311,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) {
         // centre on the parent's filtering weights m_pa (predicted location of z_i)
         g_launches.fetch_add(tc_prep_edge(p.K[i], p.Kp[i], p.D[i], p.B, in[i], ws, p.tc[i],
-                                          at<float>(ws, p.e[p.parent[i]].out), p.Kp[i], 0, s));
+                                          at<float>(ws, p.e[p.parent[i]].out), p.Kp[i], 0, p.alpha, s));
         g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/true, s));
       }
       else launch_pass(a, /*zrows=*/true, 0, dense != nullptr, s);
@@ -316,34 +322,64 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
                                                      at<float>(ws, p.lse), logp);
     TMC_COUNT_LAUNCH();
   } else {
+    // Leaves -> roots by height (height 0 = leaf); the edges of one height are independent, so
+    // their tensor-core contractions (same D) run as ONE batched persistent launch.
+    std::vector<int> height(p.n, 0);
+    int maxh = 0;
     for (int i = p.n - 1; i >= 0; --i) {
-      // h_i = u_i + sum of child messages
-      const std::vector<int>& ch = p.children[i];
-      int done = 0;
-      do {
-        HBuild hb{};
-        hb.B = p.B; hb.K = p.K[i];
-        hb.u = done == 0 ? at<float>(ws, p.u[i]) : at<float>(ws, p.e[i].h);
-        hb.uoff = done == 0 ? at<double>(ws, p.uoff[i]) : at<double>(ws, p.e[i].hoff);
-        hb.nchild = std::min<int>(kMaxChildren, (int)ch.size() - done);
-        for (int j = 0; j < hb.nchild; ++j) {
-          hb.msg[j] = at<float>(ws, p.e[ch[done + j]].out);
-          hb.moff[j] = at<double>(ws, p.e[ch[done + j]].off);
+      for (int c : p.children[i]) height[i] = std::max(height[i], height[c] + 1);
+      maxh = std::max(maxh, height[i]);
+    }
+    for (int h = 0; h <= maxh; ++h) {
+      std::vector<int> level;
+      for (int i = p.n - 1; i >= 0; --i)
+        if (height[i] == h) level.push_back(i);
+      std::vector<PassArgs> tcA;
+      std::vector<const TcLatentBuf*> tcT;
+      int tcD = 0;
+      std::vector<PrepJob> prepJ;
+      auto flush_tc = [&]() {
+        if (!tcA.empty()) {
+          g_launches.fetch_add(tc_prep_batch(prepJ.data(), (int)prepJ.size(), p.B, ws, s));
+          g_launches.fetch_add(tc_pass_forward_batch(tcA.data(), tcT.data(), (int)tcA.size(), ws, false, s));
         }
-        hb.h = at<float>(ws, p.e[i].h);
-        hb.hoff = at<double>(ws, p.e[i].hoff);
-        simt::hbuild_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(hb);
-    TMC_COUNT_LAUNCH();
-        done += hb.nchild;
-      } while (done < (int)ch.size());
-      PassArgs a = edge_args(p, i, in, dense, ws);
-      if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) {
-        // centre on softmax(h_i): z_i weighted by its subtree evidence
-        g_launches.fetch_add(tc_prep_edge(p.K[i], p.Kp[i], p.D[i], p.B, in[i], ws, p.tc[i],
-                                          at<float>(ws, p.e[i].h), p.K[i], 1, s));
-        g_launches.fetch_add(tc_pass_forward(a, p.tc[i], ws, /*zrows=*/false, s));
+        tcA.clear();
+        tcT.clear();
+        prepJ.clear();
+      };
+      for (int i : level) {
+        // h_i = u_i + sum of child messages
+        const std::vector<int>& ch = p.children[i];
+        int done = 0;
+        do {
+          HBuild hb{};
+          hb.B = p.B; hb.K = p.K[i];
+          hb.u = done == 0 ? at<float>(ws, p.u[i]) : at<float>(ws, p.e[i].h);
+          hb.uoff = done == 0 ? at<double>(ws, p.uoff[i]) : at<double>(ws, p.e[i].hoff);
+          hb.nchild = std::min<int>(kMaxChildren, (int)ch.size() - done);
+          for (int j = 0; j < hb.nchild; ++j) {
+            hb.msg[j] = at<float>(ws, p.e[ch[done + j]].out);
+            hb.moff[j] = at<double>(ws, p.e[ch[done + j]].off);
+          }
+          hb.h = at<float>(ws, p.e[i].h);
+          hb.hoff = at<double>(ws, p.e[i].hoff);
+          simt::hbuild_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(hb);
+          TMC_COUNT_LAUNCH();
+          done += hb.nchild;
+        } while (done < (int)ch.size());
+        PassArgs a = edge_args(p, i, in, dense, ws);
+        if (p.prec == TMC_PREC_TC && tc_edge_ok(p.tc[i])) {
+          // centre on softmax(h_i): z_i weighted by its subtree evidence
+          if (!tcA.empty() && tcD != p.D[i]) flush_tc();
+          tcD = p.D[i];
+          tcA.push_back(a);
+          tcT.push_back(&p.tc[i]);
+          prepJ.push_back(PrepJob{p.K[i], p.Kp[i], p.D[i], &in[i], &p.tc[i], at<float>(ws, p.e[i].h), p.K[i], 1, p.alpha});
+        } else {
+          launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
+        }
       }
-      else launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
+      flush_tc();
     }
     RootList rl{};
     rl.B = p.B;
@@ -394,28 +430,59 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
     for (int j = 0; j < rl.count; ++j) rl.w[j] = at<float>(ws, p.e[p.roots[j]].w);
     simt::final_up_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, dlogp);
     TMC_COUNT_LAUNCH();
+    // Roots -> leaves by depth: an edge's row-owner pass needs its parent edge's column sums;
+    // the edges of one depth are independent and run batched (same D) on tensor cores.
+    std::vector<int> depth(p.n, 0);
+    int maxd = 0;
     for (int i = 0; i < p.n; ++i) {
-      PassArgs a = edge_args(p, i, in, dense, ws);
-      tmc_latent_grad g = grad(i);
-      a.w = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].colsum) : at<float>(ws, p.e[i].w);
-      // row owner (param side): dmu_i, dlogvar_i, pair marginals
-      a.gmu = g.dmu; a.glv = g.dlogvar;
-      a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
-      const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
-      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, false, 1, s));
-      else launch_pass(a, false, 1, dense != nullptr, s);
-      // column owner (z side): colsum = pi_i, dz_i
-      a.gmu = nullptr; a.glv = nullptr; a.pair = nullptr;
-      a.gz = g.dz;
-      a.colsum = at<float>(ws, p.e[i].colsum);
-      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, false, 2, s));
-      else launch_pass(a, false, 2, dense != nullptr, s);
-      pi[i] = at<float>(ws, p.e[i].colsum);
+      depth[i] = p.parent[i] < 0 ? 0 : depth[p.parent[i]] + 1;
+      maxd = std::max(maxd, depth[i]);
+    }
+    for (int dl = 0; dl <= maxd; ++dl) {
+      std::vector<PassArgs> rowA, colA;
+      std::vector<const TcLatentBuf*> tcT;
+      std::vector<int> tcI;
+      for (int i = 0; i < p.n; ++i) {
+        if (depth[i] != dl) continue;
+        PassArgs a = edge_args(p, i, in, dense, ws);
+        tmc_latent_grad g = grad(i);
+        a.w = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].colsum) : at<float>(ws, p.e[i].w);
+        // row owner (param side): dmu_i, dlogvar_i, pair marginals
+        a.gmu = g.dmu; a.glv = g.dlogvar;
+        a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
+        PassArgs c = a;
+        // column owner (z side): colsum = pi_i, dz_i
+        c.gmu = nullptr; c.glv = nullptr; c.pair = nullptr;
+        c.gz = g.dz;
+        c.colsum = at<float>(ws, p.e[i].colsum);
+        pi[i] = at<float>(ws, p.e[i].colsum);
+        const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
+        if (tcb) {
+          rowA.push_back(a);
+          colA.push_back(c);
+          tcT.push_back(&p.tc[i]);
+          tcI.push_back(i);
+        } else {
+          launch_pass(a, false, 1, dense != nullptr, s);
+          launch_pass(c, false, 2, dense != nullptr, s);
+        }
+      }
+      // batched tensor-core passes, grouped by D (row-owner passes of the level, then column owners)
+      for (int Dv : {32, 64}) {
+        std::vector<PassArgs> ra, ca;
+        std::vector<const TcLatentBuf*> tt;
+        for (size_t k = 0; k < tcI.size(); ++k)
+          if (p.D[tcI[k]] == Dv) { ra.push_back(rowA[k]); ca.push_back(colA[k]); tt.push_back(tcT[k]); }
+        if (ra.empty()) continue;
+        g_launches.fetch_add(tc_pass_backward_batch(ra.data(), tt.data(), (int)ra.size(), ws, false, 1, s));
+        g_launches.fetch_add(tc_pass_backward_batch(ca.data(), tt.data(), (int)ca.size(), ws, false, 2, s));
+      }
     }
   }
   for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
     UnaryGradBatch gb{};
     gb.B = p.B;
+    gb.alpha = p.alpha;
     gb.count = std::min(kMaxUnaryPerLaunch, p.n - i0);
     for (int j = 0; j < gb.count; ++j) {
       int i = i0 + j;

@@ -26,6 +26,7 @@ struct PassArgs {
   const double *off_cb, *off_rb;  // [B] fp64 offsets carried by cb / rb (NULL = 0)
   double *off_out;             // [B] offset of `out`
   float lnC;                   // ln(#columns): the 1/K of the summed index
+  float alpha;                 // factor power: pair log-factor used = alpha * logf (1 = the TMC estimate)
   const float *w;              // [B][R] upstream gradient of out (backward)
   float *colsum;               // [B][C] sum_r P[r,c] (backward, column owner)
   float *gz, *gmu, *glv;       // owner-side gradient outputs (overwritten)
@@ -39,7 +40,7 @@ struct UnaryDesc {            // per-latent unary preparation
   int K;
 };
 constexpr int kMaxUnaryPerLaunch = 48;
-struct UnaryBatch { UnaryDesc d[kMaxUnaryPerLaunch]; int count; int B; };
+struct UnaryBatch { UnaryDesc d[kMaxUnaryPerLaunch]; int count; int B; float alpha; };
 
 constexpr int kMaxChildren = 24;
 struct HBuild {               // h_i = u_i + sum_children msg_j   (UP direction)
@@ -50,7 +51,7 @@ struct HBuild {               // h_i = u_i + sum_children msg_j   (UP direction)
 };
 
 struct UnaryGradDesc { const float *pi; float *dlogq, *dlogobs; int K; };
-struct UnaryGradBatch { UnaryGradDesc d[kMaxUnaryPerLaunch]; int count; int B; };
+struct UnaryGradBatch { UnaryGradDesc d[kMaxUnaryPerLaunch]; int count; int B; float alpha; };
 
 constexpr int kMaxRoots = 16;
 struct RootList { const float *out[kMaxRoots]; const double *off[kMaxRoots]; float *w[kMaxRoots]; int count; int B; };

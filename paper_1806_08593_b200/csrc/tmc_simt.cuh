@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
           }
           g = (OWNER_Z ? sbeta[sl] : obeta[ol]) - 0.5f * q;
         }
+        g *= a.alpha;
         if (MODE == 0) {
           float x = g + ss0[sl] - cbmax;
           if (x > lm[j]) { ls[j] = ls[j] * __expf(lm[j] - x) + 1.f; lm[j] = x; }
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
           if (wr != 0.f && el > -INFINITY) P = wr * __expf(g + cbv - cbmax - el);
           pbuf[(warp * kOPW + j) * kTC + sl] = P;
           ptot[j] += P;
-          if (MODE == 1 && a.pair) a.pair[((int64_t)b * a.Kz + ai) * a.Kp + pi] = P;
+          if (MODE == 1 && a.pair) a.pair[((int64_t)b * a.Kz + ai) * a.Kp + pi] = a.alpha * P;
         }
       }
     }
@@ -306,11 +307,11 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
         const int d = lane + 32 * q;
         if (d >= D) continue;
         if (OWNER_Z) {
-          if (a.gz) a.gz[((int64_t)b * a.Kz + o) * D + d] = acc0[j][q];
+          if (a.gz) a.gz[((int64_t)b * a.Kz + o) * D + d] = a.alpha * acc0[j][q];
         } else {
           const float lam = ov1[ol * SD + d];
-          if (a.gmu) a.gmu[((int64_t)b * a.Kp + o) * D + d] = lam * acc0[j][q];
-          if (a.glv) a.glv[((int64_t)b * a.Kp + o) * D + d] = 0.5f * (lam * acc1[j][q] - tot);
+          if (a.gmu) a.gmu[((int64_t)b * a.Kp + o) * D + d] = a.alpha * lam * acc0[j][q];
+          if (a.glv) a.glv[((int64_t)b * a.Kp + o) * D + d] = a.alpha * 0.5f * (lam * acc1[j][q] - tot);
         }
       }
     }
@@ -340,12 +341,13 @@ __global__ void __launch_bounds__(256) unary_prep_kernel(const UnaryBatch ub) {
     m = red[31];
   }
   const float shift = (m == -INFINITY) ? 0.f : m;
+  const float al = ub.alpha;
   for (int k = tid; k < d.K; k += 256) {
     float v = d.logobs ? d.logobs[(int64_t)b * d.K + k] - shift : 0.f;
     if (d.logq) v -= d.logq[(int64_t)b * d.K + k];
-    d.u[(int64_t)b * d.K + k] = v;
+    d.u[(int64_t)b * d.K + k] = al * v;
   }
-  if (tid == 0) d.uoff[b] = (double)shift;
+  if (tid == 0) d.uoff[b] = (double)al * (double)shift;
 }
 
 // h_i = u_i + sum_j msg_{j->i}  (UP direction), offsets added in fp64.
@@ -432,7 +434,7 @@ __global__ void unary_grad_kernel(const UnaryGradBatch g) {
   const UnaryGradDesc& d = g.d[blockIdx.y];
   const int64_t n = (int64_t)g.B * d.K;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float p = d.pi[i];
+    float p = g.alpha * d.pi[i];
     if (d.dlogobs) d.dlogobs[i] = p;
     if (d.dlogq) d.dlogq[i] = -p;
   }
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256) root_down_fwd_kernel(const PassArgs a) {
       s += df * df * __expf(-v) + v + kLog2Pi;
     }
   }
-  const float e = (cb0 == -INFINITY) ? -INFINITY : -0.5f * s + (cb0 - cbmax);
+  const float e = (cb0 == -INFINITY) ? -INFINITY : -0.5f * a.alpha * s + (cb0 - cbmax);
   a.ell[(int64_t)b * a.R + r] = e;
   const float rb = a.rb ? a.rb[(int64_t)b * a.R + r] : 0.f;
   a.out[(int64_t)b * a.R + r] = rb + e - a.lnC;
@@ -522,7 +524,7 @@ __global__ void __launch_bounds__(256) root_down_row_kernel(const PassArgs a) {
   const int b = (int)(idx / a.R), r = (int)(idx % a.R);
   const int D = a.D;
   const float e = a.ell[(int64_t)b * a.R + r];
-  const float P = (e == -INFINITY) ? 0.f : a.w[(int64_t)b * a.R + r];
+  const float P = (e == -INFINITY) ? 0.f : a.alpha * a.w[(int64_t)b * a.R + r];   // alpha * dJ/d(alpha logf)
   if (a.pair) a.pair[(int64_t)b * a.R + r] = P;
   if (!a.gz) return;
   const float* mu = a.mu + (int64_t)b * D;
@@ -585,8 +587,8 @@ __global__ void __launch_bounds__(256) root_down_col_kernel(const PassArgs a) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) { sm += red[0][k][lane]; sv += red[1][k][lane]; }
       if (d < D) {
-        if (a.gmu) a.gmu[(int64_t)b * D + d] = sm;
-        if (a.glv) a.glv[(int64_t)b * D + d] = 0.5f * sv;
+        if (a.gmu) a.gmu[(int64_t)b * D + d] = a.alpha * sm;
+        if (a.glv) a.glv[(int64_t)b * D + d] = a.alpha * 0.5f * sv;
       }
       if (d0 == 0) {
         float sp = 0.f;

@@ -18,6 +18,7 @@
 //                          into double-buffered TMEM accumulators, 4*RB softmax warps drain TMEM
 //                          with tcgen05.ld and run the online-max log2-sum-exp2 (ex2.approx, MUFU).
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <cstdlib>
 #include <cstdint>
@@ -234,6 +235,7 @@ struct PrepArgs {
   const float* wsrc;          // [B][wlen] log-weights of the centering mean (messages), or NULL
   int wlen;
   int wz;                     // 1: s = sum_a softmax(wsrc)[a] z[a] ; 0: s = sum_c softmax(wsrc)[c] mu[c]
+  float alpha;                // factor power: Y and beta scaled by alpha (S becomes alpha * S)
 };
 
 // hi/lo fp16 split of x (exact sum to ~2^-22 relative); lo may be subnormal.
@@ -246,8 +248,12 @@ __device__ __forceinline__ void split16(float x, __half& hi, __half& lo) {
 // pass has already weighted (UP: softmax(h_i) over z_i; DOWN: softmax(m_pa) over mu_i), else mean_c mu.
 // Any s is exact algebra; a posterior-centred s keeps the expanded terms of the pairs that carry
 // weight small, so the fp32 tensor-core accumulator never holds large cancelling partial sums.
+constexpr int kMaxPrepBatch = 16;
+struct PrepBatch { PrepArgs e[kMaxPrepBatch]; int ne; };
+
 template <int D>
-__global__ void __launch_bounds__(256) tc_shift_kernel(const PrepArgs p) {
+__global__ void __launch_bounds__(256) tc_shift_kernel(const __grid_constant__ PrepBatch pb) {
+  const PrepArgs& p = pb.e[blockIdx.z];
   const int b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ float s_part[256];
@@ -309,8 +315,10 @@ __global__ void __launch_bounds__(256) tc_shift_kernel(const PrepArgs p) {
 // K1b: operand tile images of rows [blockIdx.y * 256, +256) of both sides (Y rows then X rows
 // share the grid: y < KpPad/256 -> param rows, else z rows).
 template <int D>
-__global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
+__global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ PrepBatch pb) {
   using G = Geo<D>;
+  const PrepArgs& p = pb.e[blockIdx.z];
+  if ((int)blockIdx.y >= p.KpPad / 256 + p.KzPad / 256) return;
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ float s_shift[D];
@@ -367,10 +375,10 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
         const float lam = __expf(-vv[e]);
         const float mp = mm[e] - sh[e];
         if (j < HC) {
-          y[e] = -0.5f * lam * kLog2E;
+          y[e] = -0.5f * p.alpha * lam * kLog2E;
           bsum += lam * mp * mp + vv[e] + kLog2Pi;
         } else {
-          y[e] = lam * mp * kLog2E;
+          y[e] = p.alpha * lam * mp * kLog2E;
         }
       }
     } else {
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const PrepArgs p) {
     // beta: sum over the HC first-half chunk-threads of the row (lane groups of CPR)
 #pragma unroll
     for (int o = CPR / 2; o; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
-    if (j == 0 && c < p.KpPad) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * bsum : 0.f;
+    if (j == 0 && c < p.KpPad) p.beta[(size_t)b * p.KpPad + c] = (c < p.Kp) ? -0.5f * p.alpha * bsum : 0.f;
   }
   // z rows -> X tile image
   if (!yside)
@@ -419,7 +427,10 @@ struct ColbiasArgs {
   double* off_out;
 };
 
-__global__ void __launch_bounds__(256) tc_colbias_kernel(const ColbiasArgs a) {
+struct ColbiasBatch { ColbiasArgs e[16]; int ne; };
+
+__global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__ ColbiasBatch cbb_) {
+  const ColbiasArgs& a = cbb_.e[blockIdx.y];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[32];
   __shared__ int s_live[64];
@@ -487,8 +498,23 @@ struct FwdArgs {
   int dbg;                     // experiment flags (TMC_DEBUG_FLAGS; 0 in production): 1 no MMA, 2 no softmax math
 };
 
+// Several independent edges (siblings of a tree level) in one persistent launch: unit u belongs to
+// edge e with ustart[e] <= u < ustart[e+1].  All edges of a batch share D.
+constexpr int kMaxBatch = 16;
+struct FwdBatch {
+  FwdArgs e[kMaxBatch];
+  int ustart[kMaxBatch + 1];
+  int ne;
+};
+template <typename Batch>
+__device__ __forceinline__ int batch_edge(const Batch& fb, int u) {
+  int e = 0;
+  while (e + 1 < fb.ne && u >= fb.ustart[e + 1]) ++e;
+  return e;
+}
+
 template <int D, int NPOLY, bool MAXFREE>
-__global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArgs a) {
+__global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid_constant__ FwdBatch fb) {
   using G = Geo<D>;
   constexpr int RB = G::RB, ST = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -510,8 +536,14 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 4 * ST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int groups = a.a_tiles / RB;
-  const int units = a.B * groups;
+  const int units = fb.ustart[fb.ne];
+#define TMC_FWD_UNIT()                                                   \
+  const int e_ = batch_edge(fb, u);                                      \
+  const FwdArgs& a = fb.e[e_];                                           \
+  const int groups = a.a_tiles / RB;                                     \
+  const int uu_ = u - fb.ustart[e_];                                     \
+  const int b = uu_ / groups, g = uu_ % groups;                          \
+  (void)b; (void)g
 
   if (tid == 0) {
     mbar_init(a_full, 1);
@@ -547,7 +579,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     if (lane == 0) {
       uint32_t t = 0, ua = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        const int b = u / groups, g = u % groups;
+        TMC_FWD_UNIT();
         TMC_PROF_WAIT(true, 2, mbar_wait(a_empty, (ua & 1) ^ 1));
         mbar_expect_tx(a_full, RB * G::TILE);
         bulk_g2s(sA, a.At + ((size_t)b * a.a_tiles + (size_t)g * RB) * G::TILE, RB * G::TILE, a_full);
@@ -569,6 +601,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
       uint32_t t = 0, ua = 0;
       const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB), axBase = smem_u32(sAx), bxBase = smem_u32(sBx);
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        TMC_FWD_UNIT();
         TMC_PROF_WAIT(lane == 0, 6, mbar_wait(a_full, ua & 1));
         for (int j = 0; j < a.b_tiles; ++j, ++t) {
           const int s = t % ST, as = t & 1;
@@ -621,7 +654,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     const int rloc = rb * 128 + quarter * 32 + lane;
     uint32_t t = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int b = u / groups, g = u % groups;
+      TMC_FWD_UNIT();
       float mref = -INFINITY, sum = 0.f;
       for (int j = 0; j < a.b_tiles; ++j, ++t) {
         const int as = t & 1;
@@ -721,6 +754,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const FwdArg
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G::TMEM_COLS));
   }
 }
+#undef TMC_FWD_UNIT
 
 
 // ------------------------------------------------------------------------------ K4: reverse pass
@@ -742,6 +776,7 @@ struct BwdArgs {
   const float* ho;             // [B][o_tiles*128] owned log2 term
   const float* ht;             // [B][t_tiles*128] streamed log2 term (-inf padded)
   const float* sgn;            // [B] signed scale of the upstream weights (w = sgn * |w|/|sgn|)
+  float alpha;                 // factor power (param-side gradients scale by alpha; the Y tiles carry it already)
   int M, B;
   int owner_z;                 // 1: G = sum P Y -> dz ; 0: G = sum P X -> dmu, dlogvar
   const float *z, *mu, *lv;    // owner-side fp32 inputs [B][M][D]
@@ -817,8 +852,17 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 //   packed forms, where one MMA of N = 4D reads the streamed tile's hi and lo parts side by side
 //   ([T_hi | T_lo] is exactly the tile image seen MN-major with LBO = one atom) and the epilogue adds
 //   the two column halves:  4 = P_hi [T_hi | T_lo],  5 = (P_hi + P_lo) [T_hi | T_lo].
-template <int D, int GT>
-__global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdArgs a) {
+struct BwdBatch {
+  BwdArgs e[kMaxBatch];
+  int ustart[kMaxBatch + 1];
+  int ne;
+};
+
+// SG = softmax groups: 1 = all 16 softmax warps on every tile (one 32-column quarter each);
+// 2 = two groups of 8 alternating tiles (each warp two 32-column quarters), so two tiles are in
+// the softmax stage at once and the S -> P~ -> gradient-GEMM handoffs of one group overlap the other.
+template <int D, int GT, int SG>
+__global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __grid_constant__ BwdBatch fb) {
   using G = BGeo<D>;
   constexpr int ST = G::ST, SMW = G::SMW, EW = G::EW;
   constexpr int W_PROD = SMW + EW, W_MMA = SMW + EW + 1;     // role warps take the highest ids
@@ -856,19 +900,24 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19 + 4 * ST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int units = a.B * a.o_tiles;
+  const int units = fb.ustart[fb.ne];
   // Exact sparsity: a tile whose owner rows (or streamed rows) all carry weight exactly 0 has
   // P~ == 0 everywhere, so every role skips it consistently (phase counters count live work only).
-  auto olive = [&](int b, int mt) -> bool { return !a.olive || a.olive[(size_t)b * a.o_tiles + mt]; };
-  auto tlive = [&](int b, int j) -> bool { return !a.tlive || a.tlive[(size_t)b * a.t_tiles + j]; };
+  auto olive = [](const BwdArgs& a, int b, int mt) -> bool { return !a.olive || a.olive[(size_t)b * a.o_tiles + mt]; };
+  auto tlive = [](const BwdArgs& a, int b, int j) -> bool { return !a.tlive || a.tlive[(size_t)b * a.t_tiles + j]; };
+#define TMC_BWD_UNIT()                                                   \
+  const int e_ = batch_edge(fb, u);                                      \
+  const BwdArgs& a = fb.e[e_];                                           \
+  const int uu_ = u - fb.ustart[e_];                                     \
+  const int b = uu_ / a.o_tiles, mt = uu_ % a.o_tiles
   if (tid == 0) {
     mbar_init(o_full, 1);
     mbar_init(o_empty, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
-      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMW);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMW / SG);
     }
-    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMW); }
+    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMW / SG); }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&g_full[s], 1); mbar_init(&g_empty[s], EW);
       mbar_init(&r_full[s], SMW); mbar_init(&r_empty[s], EW);
@@ -889,14 +938,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     if (lane == 0) {   // ---------------- producer
       uint32_t t = 0, ua = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / a.o_tiles, mt = u % a.o_tiles;
-        if (!olive(b, mt)) continue;
+        TMC_BWD_UNIT();
+        if (!olive(a, b, mt)) continue;
         TMC_PROF_WAIT(true, 2, mbar_wait(o_empty, (ua & 1) ^ 1));
         ++ua;
         mbar_expect_tx(o_full, G::TILE);
         bulk_g2s(sO, a.Ot + ((size_t)b * a.o_tiles + mt) * G::TILE, G::TILE, o_full);
         for (int j = 0; j < a.t_tiles; ++j) {
-          if (!tlive(b, j)) continue;
+          if (!tlive(a, b, j)) continue;
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
           TMC_PROF_WAIT(true, 0, mbar_wait(&t_empty[s], ph));
@@ -921,7 +970,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
 #endif
       uint32_t t = 0, ua = 0;
       const uint32_t oBase = smem_u32(sO), tBase = smem_u32(sT);
-      auto grad = [&](uint32_t tt, bool first) {
+      auto grad = [&](const BwdArgs& a, uint32_t tt, bool first) {
         const uint32_t as = tt % NSB;
         const uint32_t gb = ua % GB;
         TMC_PROF_WAIT_M(5, mbar_wait(&p_full[as], (tt / NSB) & 1));
@@ -955,12 +1004,12 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         TMC_PROF_END_M(16, _tc);
       };
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int b = u / a.o_tiles, mt = u % a.o_tiles;
-        if (!olive(b, mt)) continue;
+        TMC_BWD_UNIT();
+        if (!olive(a, b, mt)) continue;
         TMC_PROF_WAIT_M(6, mbar_wait(o_full, ua & 1));
         int jj = 0;                      // live streamed tiles so far in this unit
         for (int j = 0; j < a.t_tiles; ++j) {
-          if (!tlive(b, j)) continue;
+          if (!tlive(a, b, j)) continue;
           const int s = t % ST, as = t % NSB;
           TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
           TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
@@ -989,11 +1038,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
           TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
           TMC_PROF_END_M(18, _tc2);
-          if (jj > 0) grad(t - 1, jj == 1);
+          if (jj > 0) grad(a, t - 1, jj == 1);
           ++jj;
           ++t;
         }
-        if (jj > 0) grad(t - 1, jj == 1);
+        if (jj > 0) grad(a, t - 1, jj == 1);
         mma_commit(&g_full[ua % GB]);
         mma_commit(o_empty);
         ++ua;
@@ -1012,82 +1061,85 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     // columns another warp still has to read.
     const int sw = warp;
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
-    const int cq = sw >> 2;                     // column quarter of the tile
+    const int grp = (SG == 2) ? (sw >> 3) : 0;  // tile parity this warp processes (SG = 2)
+    const int slot = (SG == 2) ? ((sw >> 2) & 1) : (sw >> 2);   // row-sum slot (4 per row)
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int b = u / a.o_tiles, mt = u % a.o_tiles;
-      if (!olive(b, mt)) continue;
+      TMC_BWD_UNIT();
+      if (!olive(a, b, mt)) continue;
       const int gm = mt * 128 + m;
       const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
       const float2 hom2 = make_float2(hom, hom);
       float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       for (int j = 0; j < a.t_tiles; ++j) {
-        if (!tlive(b, j)) continue;
+        if (!tlive(a, b, j)) continue;
+        if (SG == 2 && (int)(t & 1) != grp) { ++t; continue; }
         const int as = t % NSB, s = t % ST;
         TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
-        uint32_t v[32];
-        const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
-        TMC_PROF_T0(_tl);
-        if (!(a.dbg & 16)) {     // experiment flag 16: no TMEM traffic from the softmax warps
-          TMC_LD32(taddr, v);
-          tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = 0u;
-        }
-        TMC_PROF_END(sw == 0 && lane == 0, 19, _tl);
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
-        const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
-        uint32_t hi[16], lo[16];
-        if (hom > -INFINITY && !(a.dbg & 4)) {
+#pragma unroll 1
+        for (int c = 0; c < (SG == 2 ? 2 : 1); ++c) {
+          // column quarter handled now: 32 S columns; P~ hi/lo go back into the same 32 columns
+          const int cq = (SG == 2) ? (((sw >> 2) & 1) * 2 + c) : (sw >> 2);
+          uint32_t v[32];
+          const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
+          if (!(a.dbg & 16)) {     // experiment flag 16: no TMEM traffic from the softmax warps
+            TMC_LD32(taddr, v);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 h4 = hts[q];
-            // arguments on packed pairs: S + ht + (ho + 14)
-            const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
-                                                     make_float2(h4.x, h4.y)), hom2);
-            const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
-                                                     make_float2(h4.z, h4.w)), hom2);
-            const float2 p01 = make_float2(ex2(y01.x), ex2(y01.y)), p23 = make_float2(ex2(y23.x), ex2(y23.y));
-            racc[0] = __fadd2_rn(racc[0], p01);
-            racc[1] = __fadd2_rn(racc[1], p23);
-            __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
-            hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
-            hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
-            if constexpr (PLO) {
-              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-              const float2 d01 = __fadd2_rn(p01, make_float2(-f01.x, -f01.y));
-              const float2 d23 = __fadd2_rn(p23, make_float2(-f23.x, -f23.y));
-              __half2 l01 = __floats2half2_rn(d01.x, d01.y), l23 = __floats2half2_rn(d23.x, d23.y);
-              lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
-              lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
-            }
+            for (int q = 0; q < 32; ++q) v[q] = 0u;
           }
-        } else {
+          const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
+          uint32_t hi[16], lo[16];
+          if (hom > -INFINITY && !(a.dbg & 4)) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
+            for (int q = 0; q < 8; ++q) {
+              const float4 h4 = hts[q];
+              // arguments on packed pairs: S + ht + (ho + 14)
+              const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
+                                                       make_float2(h4.x, h4.y)), hom2);
+              const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
+                                                       make_float2(h4.z, h4.w)), hom2);
+              const float2 p01 = make_float2(ex2(y01.x), ex2(y01.y)), p23 = make_float2(ex2(y23.x), ex2(y23.y));
+              racc[0] = __fadd2_rn(racc[0], p01);
+              racc[1] = __fadd2_rn(racc[1], p23);
+              __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
+              hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
+              hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
+              if constexpr (PLO) {
+                const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+                const float2 d01 = __fadd2_rn(p01, make_float2(-f01.x, -f01.y));
+                const float2 d23 = __fadd2_rn(p23, make_float2(-f23.x, -f23.y));
+                __half2 l01 = __floats2half2_rn(d01.x, d01.y), l23 = __floats2half2_rn(d23.x, d23.y);
+                lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
+                lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
+          }
+          if (!(a.dbg & 16)) {
+            TMC_ST16(taddr, hi);
+            if constexpr (PLO) TMC_ST16(taddr + 16, lo);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&h_empty[s]);
-        TMC_PROF_T0(_tst);
-        if (!(a.dbg & 16)) {
-          TMC_ST16(taddr, hi);
-          if constexpr (PLO) TMC_ST16(taddr + 16, lo);
-          tmem_st_wait();
-        }
+        if (!(a.dbg & 16)) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
-        TMC_PROF_END(sw == 0 && lane == 0, 20, _tst);
         ++t;
       }
-      // this column quarter's row sums -> the epilogue warps
+      // this warp's row sums -> the epilogue warps
       mbar_wait(&r_empty[ua & 1], ((ua >> 1) & 1) ^ 1);
       const float2 rr = __fadd2_rn(racc[0], racc[1]);
-      sRs[(ua & 1) * 512 + cq * 128 + m] = rr.x + rr.y;
+      sRs[(ua & 1) * 512 + (grp * 2 + slot) % 4 * 128 + m] = rr.x + rr.y;
       __syncwarp();
       if (lane == 0) mbar_arrive(&r_full[ua & 1]);
       ++ua;
@@ -1101,9 +1153,9 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t ua = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int b = u / a.o_tiles, mt = u % a.o_tiles;
+      TMC_BWD_UNIT();
       const int gm = mt * 128 + m;
-      if (!olive(b, mt)) {
+      if (!olive(a, b, mt)) {
         // no owner row carries weight: every gradient of these rows is exactly 0
         if (gm < a.M) {
           const size_t row = ((size_t)b * a.M + gm) * D;
@@ -1121,7 +1173,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
         continue;
       }
       int nl = 0;
-      for (int j = 0; j < a.t_tiles; ++j) nl += tlive(b, j) ? 1 : 0;
+      for (int j = 0; j < a.t_tiles; ++j) nl += tlive(a, b, j) ? 1 : 0;
       const uint32_t gb = ua % GB;
       mbar_wait(&r_full[ua & 1], (ua >> 1) & 1);
       const float* rs = sRs + (ua & 1) * 512;
@@ -1189,8 +1241,8 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
               const float mp = mm[e] - sh[d0 + d4 + e];
               const float lam = __expf(-vv[e]);
               const float A1 = g1[d4 + e] * sc, A2 = g0[d4 + e] * sc;
-              om[e] = lam * (A1 - mp * pi);
-              ov[e] = 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+              om[e] = a.alpha * lam * (A1 - mp * pi);
+              ov[e] = a.alpha * 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
             }
             if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d0 + d4) = make_float4(om[0], om[1], om[2], om[3]);
             if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d0 + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
@@ -1211,6 +1263,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const BwdAr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
+#undef TMC_BWD_UNIT
 
 // Per-row terms of the reverse pass: rterm2[r] = log2(|w[r]|/ws) - (ell[r] - beta[r]) log2e (-inf when
 // the row carries no weight) and sgn[b] = +-ws, where ws = 2^ceil(log2 max_r |w[r]|) keeps the fp16
@@ -1224,7 +1277,10 @@ struct RowtermArgs {
   int* live;                     // [B][Rpad/128] 1 if any row of the 128-row tile carries weight
 };
 
-__global__ void __launch_bounds__(256) tc_rowterm_kernel(const RowtermArgs a) {
+struct RowtermBatch { RowtermArgs e[16]; int ne; };
+
+__global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__ RowtermBatch rb_) {
+  const RowtermArgs& a = rb_.e[blockIdx.y];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[8];
   __shared__ int neg;
@@ -1278,6 +1334,8 @@ inline bool tc_dense_reverse() {
 
 // Default number of fp16 terms of the reverse pass's gradient GEMM (TMC_BWD_GRAD_TERMS overrides).
 constexpr int kDefaultGradTerms = 3;
+// Default softmax grouping of the reverse pass (TMC_BWD_SG overrides).
+constexpr int kDefaultBwdGroups = 1;
 
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
@@ -1336,27 +1394,55 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
 inline bool tc_edge_ok(const TcLatentBuf& b) { return b.ok; }
 
 template <int D>
-inline void tc_prep_launch(const tc::PrepArgs& p, int B, cudaStream_t s) {
-  tc::tc_shift_kernel<D><<<B, 256, 0, s>>>(p);
-  tc::tc_prep_kernel<D><<<dim3(B, p.KpPad / 256 + p.KzPad / 256), 256, 0, s>>>(p);
+inline void tc_prep_launch(const tc::PrepBatch& pb, int B, cudaStream_t s) {
+  int chunks = 0;
+  for (int k = 0; k < pb.ne; ++k) chunks = std::max(chunks, pb.e[k].KpPad / 256 + pb.e[k].KzPad / 256);
+  tc::tc_shift_kernel<D><<<dim3(B, 1, pb.ne), 256, 0, s>>>(pb);
+  tc::tc_prep_kernel<D><<<dim3(B, chunks, pb.ne), 256, 0, s>>>(pb);
 }
 
-// Operand prep of one tensor-core edge (latent i): X/Y tile images, beta and the centering shift.
-// wsrc/wlen/wz: the message weights the shift is centred on (see tc_prep_kernel).
+// Operand prep of tensor-core edges (one launch pair for up to kMaxPrepBatch edges of equal D):
+// X/Y tile images, beta and the centering shift.  wsrc/wlen/wz: the message weights each edge's
+// shift is centred on (see tc_shift_kernel).
+struct PrepJob {
+  int Ki, Kpi, Di;
+  const tmc_latent_in* in;
+  const TcLatentBuf* t;
+  const float* wsrc;
+  int wlen, wz;
+  float alpha;
+};
+
+inline int tc_prep_batch(const PrepJob* jobs, int ne, int B, void* ws, cudaStream_t s) {
+  if (B == 0 || ne == 0) return 0;
+  int launched = 0;
+  for (int e0 = 0; e0 < ne; e0 += tc::kMaxPrepBatch) {
+    tc::PrepBatch pb{};
+    pb.ne = std::min(tc::kMaxPrepBatch, ne - e0);
+    for (int k = 0; k < pb.ne; ++k) {
+      const PrepJob& j = jobs[e0 + k];
+      tc::PrepArgs& p = pb.e[k];
+      p.z = j.in->z; p.mu = j.in->mu; p.lv = j.in->logvar;
+      p.Kz = j.Ki; p.Kp = j.Kpi; p.KzPad = j.t->KzPad; p.KpPad = j.t->KpPad;
+      p.Xt = static_cast<uint8_t*>(ws) + j.t->xt;
+      p.Yt = static_cast<uint8_t*>(ws) + j.t->yt;
+      p.beta = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + j.t->beta);
+      p.shift = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + j.t->shift);
+      p.wsrc = j.wsrc; p.wlen = j.wlen; p.wz = j.wz;
+      p.alpha = j.alpha;
+    }
+    if (jobs[e0].Di == 32) tc_prep_launch<32>(pb, B, s);
+    else tc_prep_launch<64>(pb, B, s);
+    launched += 2;   // shift + image kernels
+  }
+  return launched;
+}
+
 inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in, void* ws, const TcLatentBuf& t,
-                        const float* wsrc, int wlen, int wz, cudaStream_t s) {
-  if (!t.ok || B == 0) return 0;
-  tc::PrepArgs p{};
-  p.z = in.z; p.mu = in.mu; p.lv = in.logvar;
-  p.Kz = Ki; p.Kp = Kpi; p.KzPad = t.KzPad; p.KpPad = t.KpPad;
-  p.Xt = static_cast<uint8_t*>(ws) + t.xt;
-  p.Yt = static_cast<uint8_t*>(ws) + t.yt;
-  p.beta = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.beta);
-  p.shift = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + t.shift);
-  p.wsrc = wsrc; p.wlen = wlen; p.wz = wz;
-  if (Di == 32) tc_prep_launch<32>(p, B, s);
-  else tc_prep_launch<64>(p, B, s);
-  return 2;   // shift + image kernels
+                        const float* wsrc, int wlen, int wz, float alpha, cudaStream_t s) {
+  if (!t.ok) return 0;
+  PrepJob j{Ki, Kpi, Di, &in, &t, wsrc, wlen, wz, alpha};
+  return tc_prep_batch(&j, 1, B, ws, s);
 }
 
 // Forward softmax variant (TMC_FWD_VARIANT overrides):
@@ -1369,7 +1455,7 @@ inline int tc_fwd_variant() {
 }
 
 template <int D, int NPOLY, bool MF>
-inline void tc_fwd_launch_t(const tc::FwdArgs& f, cudaStream_t s) {
+inline void tc_fwd_launch_t(const tc::FwdBatch& fb, cudaStream_t s) {
   using G = tc::Geo<D>;
   static bool attr = false;
   if (!attr) {
@@ -1382,53 +1468,74 @@ inline void tc_fwd_launch_t(const tc::FwdArgs& f, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int units = f.B * (f.a_tiles / G::RB);
+  const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
-  tc::tc_fwd_kernel<D, NPOLY, MF><<<grid, G::THREADS, G::SMEM, s>>>(f);
+  if (grid > 0) tc::tc_fwd_kernel<D, NPOLY, MF><<<grid, G::THREADS, G::SMEM, s>>>(fb);
 }
 
 template <int D>
-inline void tc_fwd_launch(const tc::FwdArgs& f, cudaStream_t s) {
+inline void tc_fwd_launch(const tc::FwdBatch& fb, cudaStream_t s) {
   switch (tc_fwd_variant()) {
-    case 1: return tc_fwd_launch_t<D, 0, true>(f, s);
-    case 2: return tc_fwd_launch_t<D, 2, true>(f, s);
-    default: return tc_fwd_launch_t<D, 0, false>(f, s);
+    case 1: return tc_fwd_launch_t<D, 0, true>(fb, s);
+    case 2: return tc_fwd_launch_t<D, 2, true>(fb, s);
+    default: return tc_fwd_launch_t<D, 0, false>(fb, s);
   }
 }
 
-// Forward contraction of one edge on tensor cores.  zrows = DOWN (rows = z side).
-// Returns the number of kernels launched.
-inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, cudaStream_t s) {
+// Forward contraction of ne edges (same D) on tensor cores: per-edge column bias, then ONE persistent
+// launch over the units of every edge (siblings of a tree level run together).  zrows = DOWN (rows =
+// z side).  Returns the number of kernels launched.
+inline int tc_pass_forward_batch(const PassArgs* as, const TcLatentBuf* const* ts, int ne, void* ws, bool zrows,
+                                 cudaStream_t s) {
   uint8_t* w = static_cast<uint8_t*>(ws);
-  const int Cpad = zrows ? t.KpPad : t.KzPad;
-  tc::ColbiasArgs cbA{};
-  cbA.cb = a.cb;
-  cbA.beta = zrows ? reinterpret_cast<const float*>(w + t.beta) : nullptr;
-  cbA.betaStride = t.KpPad;
-  cbA.C = a.C; cbA.Cpad = Cpad;
-  cbA.cb2 = reinterpret_cast<float*>(w + t.cb2);
-  cbA.bx = w + t.bx;
-  cbA.live = reinterpret_cast<int*>(w + t.clive);
-  cbA.cbmax = a.cbmax;
-  cbA.off_cb = a.off_cb; cbA.off_rb = a.off_rb; cbA.off_out = a.off_out;
-  tc::tc_colbias_kernel<<<a.B, 256, 0, s>>>(cbA);
+  int launched = 0;
+  for (int e0 = 0; e0 < ne; e0 += tc::kMaxBatch) {
+    tc::FwdBatch fb{};
+    tc::ColbiasBatch cb{};
+    fb.ne = std::min(tc::kMaxBatch, ne - e0);
+    cb.ne = fb.ne;
+    fb.ustart[0] = 0;
+    for (int k = 0; k < fb.ne; ++k) {
+      const PassArgs& a = as[e0 + k];
+      const TcLatentBuf& t = *ts[e0 + k];
+      const int Cpad = zrows ? t.KpPad : t.KzPad;
+      tc::ColbiasArgs& cbA = cb.e[k];
+      cbA.cb = a.cb;
+      cbA.beta = zrows ? reinterpret_cast<const float*>(w + t.beta) : nullptr;
+      cbA.betaStride = t.KpPad;
+      cbA.C = a.C; cbA.Cpad = Cpad;
+      cbA.cb2 = reinterpret_cast<float*>(w + t.cb2);
+      cbA.bx = w + t.bx;
+      cbA.live = reinterpret_cast<int*>(w + t.clive);
+      cbA.cbmax = a.cbmax;
+      cbA.off_cb = a.off_cb; cbA.off_rb = a.off_rb; cbA.off_out = a.off_out;
+      tc::FwdArgs& f = fb.e[k];
+      f.At = zrows ? w + t.xt : w + t.yt;
+      f.Bt = zrows ? w + t.yt : w + t.xt;
+      f.a_tiles = (zrows ? t.KzPad : t.KpPad) / 128;
+      f.b_tiles = Cpad / 128;
+      f.cb2 = cbA.cb2;
+      f.Bx = cbA.bx;
+      f.ell_add = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
+      f.ell_stride = t.KpPad;
+      f.out_add = a.rb;
+      f.R = a.R; f.B = a.B; f.lnC = a.lnC;
+      f.out = a.out; f.ell = a.ell;
+      f.dbg = tc_debug_flags() & 3;
+      const int rb = (t.D == 32) ? tc::Geo<32>::RB : tc::Geo<64>::RB;
+      fb.ustart[k + 1] = fb.ustart[k] + a.B * (f.a_tiles / rb);
+    }
+    tc::tc_colbias_kernel<<<dim3(as[e0].B, cb.ne), 256, 0, s>>>(cb);
+    if (ts[e0]->D == 32) tc_fwd_launch<32>(fb, s);
+    else tc_fwd_launch<64>(fb, s);
+    launched += 2;
+  }
+  return launched;
+}
 
-  tc::FwdArgs f{};
-  f.At = zrows ? w + t.xt : w + t.yt;
-  f.Bt = zrows ? w + t.yt : w + t.xt;
-  f.a_tiles = (zrows ? t.KzPad : t.KpPad) / 128;
-  f.b_tiles = Cpad / 128;
-  f.cb2 = cbA.cb2;
-  f.Bx = cbA.bx;
-  f.ell_add = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
-  f.ell_stride = t.KpPad;
-  f.out_add = a.rb;
-  f.R = a.R; f.B = a.B; f.lnC = a.lnC;
-  f.out = a.out; f.ell = a.ell;
-  f.dbg = tc_debug_flags() & 3;
-  if (t.D == 32) tc_fwd_launch<32>(f, s);
-  else tc_fwd_launch<64>(f, s);
-  return 2;
+inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, cudaStream_t s) {
+  const TcLatentBuf* tp = &t;
+  return tc_pass_forward_batch(&a, &tp, 1, ws, zrows, s);
 }
 
 inline int tc_grad_terms() {
@@ -1437,12 +1544,18 @@ inline int tc_grad_terms() {
   return (v >= 1 && v <= 5) ? v : kDefaultGradTerms;
 }
 
-template <int D, int GT>
-inline void tc_bwd_launch_t(const tc::BwdArgs& f, cudaStream_t s) {
+inline int tc_bwd_groups() {
+  const char* e = std::getenv("TMC_BWD_SG");
+  const int v = e ? std::atoi(e) : kDefaultBwdGroups;
+  return (v == 1 || v == 2) ? v : kDefaultBwdGroups;
+}
+
+template <int D, int GT, int SG>
+inline void tc_bwd_launch_t(const tc::BwdBatch& fb, cudaStream_t s) {
   using G = tc::BGeo<D>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc::tc_bwd_kernel<D, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    cudaFuncSetAttribute(tc::tc_bwd_kernel<D, GT, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
     attr = true;
   }
   static int sms = 0;
@@ -1451,72 +1564,93 @@ inline void tc_bwd_launch_t(const tc::BwdArgs& f, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int units = f.B * f.o_tiles;
+  const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
-  tc::tc_bwd_kernel<D, GT><<<grid, G::THREADS, G::SMEM, s>>>(f);
+  if (grid > 0) tc::tc_bwd_kernel<D, GT, SG><<<grid, G::THREADS, G::SMEM, s>>>(fb);
 }
 
 template <int D>
-inline void tc_bwd_launch(const tc::BwdArgs& f, cudaStream_t s) {
+inline void tc_bwd_launch(const tc::BwdBatch& fb, cudaStream_t s) {
+  const bool two = tc_bwd_groups() == 2;
   switch (tc_grad_terms()) {
-    case 1: return tc_bwd_launch_t<D, 1>(f, s);
-    case 2: return tc_bwd_launch_t<D, 2>(f, s);
-    case 4: return tc_bwd_launch_t<D, 4>(f, s);
-    case 5: return tc_bwd_launch_t<D, 5>(f, s);
-    default: return tc_bwd_launch_t<D, 3>(f, s);
+    case 4: return two ? tc_bwd_launch_t<D, 4, 2>(fb, s) : tc_bwd_launch_t<D, 4, 1>(fb, s);
+    default: return two ? tc_bwd_launch_t<D, 3, 2>(fb, s) : tc_bwd_launch_t<D, 3, 1>(fb, s);
   }
 }
 
 inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.ok && t.bwd_ok && !a.pair; }
 
-// Reverse pass of one edge on tensor cores: row-owner pass (mode 1) or column-owner pass (mode 2).
-// The row terms are prepared once, before the row-owner pass.  Returns kernels launched.
+// Reverse pass of ne edges (same D) on tensor cores: row-owner pass (mode 1) or column-owner pass
+// (mode 2), ONE persistent launch over every edge's units.  The row terms are prepared per edge
+// before the row-owner pass.  Returns kernels launched.
+inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* ts, int ne, void* ws, bool zrows,
+                                  int mode, cudaStream_t s) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int launched = 0;
+  for (int e0 = 0; e0 < ne; e0 += tc::kMaxBatch) {
+    tc::BwdBatch fb{};
+    tc::RowtermBatch rtb{};
+    fb.ne = std::min(tc::kMaxBatch, ne - e0);
+    rtb.ne = fb.ne;
+    fb.ustart[0] = 0;
+    for (int k = 0; k < fb.ne; ++k) {
+      const PassArgs& a = as[e0 + k];
+      const TcLatentBuf& t = *ts[e0 + k];
+      const int Rpad = zrows ? t.KzPad : t.KpPad, Cpad = zrows ? t.KpPad : t.KzPad;
+      float* rterm2 = reinterpret_cast<float*>(w + t.rterm2);
+      float* sgn = reinterpret_cast<float*>(w + t.sgn);
+      if (mode == 1) {
+        tc::RowtermArgs& r = rtb.e[k];
+        r.ell = a.ell; r.w = a.w;
+        r.beta = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
+        r.betaStride = t.KpPad; r.R = a.R; r.Rpad = Rpad;
+        r.rterm2 = rterm2; r.sgn = sgn;
+        r.live = reinterpret_cast<int*>(w + t.rlive);
+      }
+      tc::BwdArgs& f = fb.e[k];
+      const bool own_rows = (mode == 1);
+      const uint8_t* rowT = zrows ? w + t.xt : w + t.yt;
+      const uint8_t* colT = zrows ? w + t.yt : w + t.xt;
+      f.Ot = own_rows ? rowT : colT;
+      f.Tt = own_rows ? colT : rowT;
+      f.o_tiles = (own_rows ? Rpad : Cpad) / 128;
+      f.t_tiles = (own_rows ? Cpad : Rpad) / 128;
+      f.ho = own_rows ? rterm2 : reinterpret_cast<const float*>(w + t.cb2);
+      f.ht = own_rows ? reinterpret_cast<const float*>(w + t.cb2) : rterm2;
+      f.sgn = sgn;
+      f.M = own_rows ? a.R : a.C;
+      f.B = a.B;
+      const bool owner_is_z = (own_rows == zrows);
+      f.owner_z = owner_is_z ? 1 : 0;
+      f.z = a.z; f.mu = a.mu; f.lv = a.lv;
+      f.shift = reinterpret_cast<const float*>(w + t.shift);
+      f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
+      f.rowsum = own_rows ? nullptr : a.colsum;
+      if (!tc_dense_reverse()) {
+        const int* rl = reinterpret_cast<const int*>(w + t.rlive);
+        const int* cl = reinterpret_cast<const int*>(w + t.clive);
+        f.olive = own_rows ? rl : cl;
+        f.tlive = own_rows ? cl : rl;
+      }
+      f.dbg = (tc_debug_flags() >> 2) & 31;
+      f.alpha = a.alpha;
+      fb.ustart[k + 1] = fb.ustart[k] + a.B * f.o_tiles;
+    }
+    if (mode == 1) {
+      tc::tc_rowterm_kernel<<<dim3(as[e0].B, rtb.ne), 256, 0, s>>>(rtb);
+      ++launched;
+    }
+    if (ts[e0]->D == 32) tc_bwd_launch<32>(fb, s);
+    else tc_bwd_launch<64>(fb, s);
+    ++launched;
+  }
+  return launched;
+}
+
 inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, int mode,
                             cudaStream_t s) {
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  const int Rpad = zrows ? t.KzPad : t.KpPad, Cpad = zrows ? t.KpPad : t.KzPad;
-  float* rterm2 = reinterpret_cast<float*>(w + t.rterm2);
-  float* sgn = reinterpret_cast<float*>(w + t.sgn);
-  int n = 0;
-  if (mode == 1) {
-    tc::RowtermArgs r{};
-    r.ell = a.ell; r.w = a.w;
-    r.beta = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
-    r.betaStride = t.KpPad; r.R = a.R; r.Rpad = Rpad;
-    r.rterm2 = rterm2; r.sgn = sgn;
-    r.live = reinterpret_cast<int*>(w + t.rlive);
-    tc::tc_rowterm_kernel<<<a.B, 256, 0, s>>>(r);
-    ++n;
-  }
-  tc::BwdArgs f{};
-  const bool own_rows = (mode == 1);
-  const uint8_t* rowT = zrows ? w + t.xt : w + t.yt;
-  const uint8_t* colT = zrows ? w + t.yt : w + t.xt;
-  f.Ot = own_rows ? rowT : colT;
-  f.Tt = own_rows ? colT : rowT;
-  f.o_tiles = (own_rows ? Rpad : Cpad) / 128;
-  f.t_tiles = (own_rows ? Cpad : Rpad) / 128;
-  f.ho = own_rows ? rterm2 : reinterpret_cast<const float*>(w + t.cb2);
-  f.ht = own_rows ? reinterpret_cast<const float*>(w + t.cb2) : rterm2;
-  f.sgn = sgn;
-  f.M = own_rows ? a.R : a.C;
-  f.B = a.B;
-  const bool owner_is_z = (own_rows == zrows);
-  f.owner_z = owner_is_z ? 1 : 0;
-  f.z = a.z; f.mu = a.mu; f.lv = a.lv;
-  f.shift = reinterpret_cast<const float*>(w + t.shift);
-  f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
-  f.rowsum = own_rows ? nullptr : a.colsum;
-  if (!tc_dense_reverse()) {
-    const int* rl = reinterpret_cast<const int*>(w + t.rlive);
-    const int* cl = reinterpret_cast<const int*>(w + t.clive);
-    f.olive = own_rows ? rl : cl;
-    f.tlive = own_rows ? cl : rl;
-  }
-  f.dbg = (tc_debug_flags() >> 2) & 31;
-  if (t.D == 32) tc_bwd_launch<32>(f, s);
-  else tc_bwd_launch<64>(f, s);
-  return n + 1;
+  const TcLatentBuf* tp = &t;
+  return tc_pass_backward_batch(&a, &tp, 1, ws, zrows, mode, s);
 }
 
 // ------------------------------------------------------------------------------ K2: tmc_factors on tensor cores

@@ -33,9 +33,9 @@ def upload(torch, wl):
             for i in range(len(wl.parent))]
 
 
-def run_gpu(torch, wl, direction=0, precision=0, dlogp=None, pair=False, grads=True):
+def run_gpu(torch, wl, direction=0, precision=0, dlogp=None, pair=False, grads=True, alpha=1.0):
     import paper_1806_08593_b200 as tmc
-    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=direction, precision=precision)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=direction, precision=precision, factor_power=alpha)
     inp = upload(torch, wl)
     dl = None if dlogp is None else torch.from_numpy(np.asarray(dlogp, np.float64)).cuda()
     logp, gr = tmc.estimate(g, inp, dlogp=dl, grads=grads, pair=pair)
@@ -262,3 +262,16 @@ def test_parity_full_size_sampled(torch_cuda, name):
     ref = oracle.estimate_workload(sub, direction="up")
     dmax, worst = compare(got, ref, b_sel=sample, tag=name)
     print(name, "max |dlogp|", dmax, "worst grad rel", max(worst.values()))
+
+
+@pytest.mark.parametrize("name,kw,pair", [("S_chain", {}, True), ("S_tree", {}, True), ("C3", dict(B=2, K=300), False),
+                                          ("C4", dict(B=2, K=130), False), ("C2", dict(B=2, K=200), False),
+                                          ("C1", dict(B=4), True)])
+def test_factor_power_two(torch_cuda, name, kw, pair):
+    """factor_power = 2: log((1/prod K) sum w^2), the DReGs surrogate's second TMC run,
+    and its gradients, on the SIMT and tensor-core paths against the oracle with alpha = 2."""
+    wl = tw.make_workload(name, **kw)
+    got = run_gpu(torch_cuda, wl, pair=pair, alpha=2.0)
+    ref = oracle.estimate_workload(wl, alpha=2.0, pair=pair)
+    keys = ("dz", "dmu", "dlogvar", "dlogq", "dlogobs") + (("pair",) if pair else ())
+    compare(got, ref, keys=keys, tag=f"{name} alpha=2")

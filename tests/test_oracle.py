@@ -13,7 +13,7 @@ from scipy.stats import multivariate_normal, norm
 
 import oracle
 import tmc_workload as tw
-from bruteforce import log_factor, pair_marginals, tmc_bruteforce, workload_datapoint
+from bruteforce import log_factor, log_weights, pair_marginals, tmc_bruteforce, workload_datapoint
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 TINY = ["S_chain", "S_tree", "S_mnist", "S_mlp", "S_mlp_bern", "C0"]
@@ -311,3 +311,73 @@ def test_dlogp_scales_gradients():
     for i in range(len(wl.parent)):
         np.testing.assert_allclose(r2["dz"][i], r1["dz"][i] * w[:, None, None], atol=1e-14)
         np.testing.assert_allclose(r2["dlogq"][i], r1["dlogq"][i] * w[:, None], atol=1e-14)
+
+
+# ----------------------------------------------------------------------------- factor power (NEXT-1)
+@pytest.mark.parametrize("name", ["S_chain", "S_tree", "S_mlp", "S_mnist"])
+def test_alpha2_is_sum_of_squared_weights(name):
+    """alpha = 2: "running TMC again, with squared weights" == log((1/prod K) sum w^2),
+    the second quantity of the DReGs surrogate, by brute-force enumeration."""
+    wl = tw.make_workload(name)
+    r = oracle.estimate_workload(wl, alpha=2.0, grads=False)
+    for b in range(wl.B):
+        fac, obs = workload_datapoint(wl, b)
+        fac2 = [2.0 * f for f in fac]
+        obs2 = [None if o is None else 2.0 * o for o in obs]
+        assert abs(r["logp"][b] - tmc_bruteforce(wl.parent, wl.K, fac2, obs2)) < 1e-10
+
+
+def test_alpha2_gradients_match_finite_differences():
+    wl = tw.make_workload("S_tree")
+    r = oracle.estimate_workload(wl, alpha=2.0)
+    h = 1e-5
+    b = 1
+
+    def val(i, which, arr):
+        fac, obs = [], []
+        for j in range(len(wl.parent)):
+            z, mu, lv, lq = wl.z[j][b], wl.mu[j][b], wl.logvar[j][b], wl.logq[j][b]
+            if j == i:
+                z = arr if which == "z" else z
+                mu = arr if which == "mu" else mu
+            fac.append(2.0 * log_factor(z, mu, lv, lq))
+            obs.append(None if wl.logobs[j] is None else 2.0 * np.asarray(wl.logobs[j][b], np.float64))
+        return tmc_bruteforce(wl.parent, wl.K, fac, obs)
+
+    for i in range(len(wl.parent)):
+        for which, src, key in (("z", wl.z, "dz"), ("mu", wl.mu, "dmu")):
+            base = src[i][b].astype(np.float64)
+            fd = np.zeros_like(base)
+            for idx in np.ndindex(base.shape):
+                e = np.zeros_like(base)
+                e[idx] = h
+                fd[idx] = (val(i, which, base + e) - val(i, which, base - e)) / (2 * h)
+            assert np.abs(r[key][i][b] - fd).max() / max(1e-3, np.abs(fd).max()) < 1e-6
+
+
+def test_dregs_surrogate_identity():
+    """d/dz of 1/2 (sum w^2 / (sum w)^2) log sum w_hat^2 equals
+    sum_i w_i^2/(sum w)^2 d log w_i / dz.  With L_a = log((1/prod K) sum w^a) from the oracle:
+    1/2 exp(L_2 - 2 L_1 - sum ln K) * dL_2/dz  ==  the brute-force weighted sum (here w.r.t. z)."""
+    wl = tw.make_workload("S_chain")
+    r1 = oracle.estimate_workload(wl, alpha=1.0, grads=False)
+    r2 = oracle.estimate_workload(wl, alpha=2.0)
+    lnK = sum(math.log(k) for k in wl.K)
+    for b in range(wl.B):
+        fac, obs = workload_datapoint(wl, b)
+        combos, lw = log_weights(wl.parent, wl.K, fac, obs)
+        c = np.exp(2 * lw - 2 * logsumexp(lw))          # w_i^2 / (sum w)^2
+        # d log w_i / d z_j[a, d]: log w_i depends on z_j[k_j] through factor j and its children
+        for j in range(len(wl.parent)):
+            g = np.zeros_like(wl.z[j][b], dtype=np.float64)
+            h = 1e-6
+            for idx in np.ndindex(g.shape):
+                zp = wl.z[j][b].astype(np.float64).copy(); zp[idx] += h
+                zm = wl.z[j][b].astype(np.float64).copy(); zm[idx] -= h
+                def lwz(zz):
+                    f2, o2 = list(fac), list(obs)
+                    f2[j] = log_factor(zz, wl.mu[j][b], wl.logvar[j][b], wl.logq[j][b])
+                    return log_weights(wl.parent, wl.K, f2, o2)[1]
+                g[idx] = np.sum(c * (lwz(zp) - lwz(zm)) / (2 * h))
+            scale = 0.5 * math.exp(r2["logp"][b] - 2 * r1["logp"][b] - lnK)
+            np.testing.assert_allclose(scale * r2["dz"][j][b], g, rtol=1e-5, atol=1e-7)
