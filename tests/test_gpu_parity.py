@@ -275,3 +275,26 @@ def test_factor_power_two(torch_cuda, name, kw, pair):
     ref = oracle.estimate_workload(wl, alpha=2.0, pair=pair)
     keys = ("dz", "dmu", "dlogvar", "dlogq", "dlogobs") + (("pair",) if pair else ())
     compare(got, ref, keys=keys, tag=f"{name} alpha=2")
+
+
+def test_dregs_gradient_matches_bruteforce(torch_cuda):
+    """NEXT-1: the TMC-DReGs recognition gradient computed with two libtmc runs
+    (factor_power 1 and 2) and the harness chain rule equals the definition
+    sum_i w_i^2/(sum w)^2 d log w_hat_i / d phi evaluated by enumerating every index tuple."""
+    from tmc_workload.torch_model import TorchModel, dregs_step
+    torch = torch_cuda
+    wl = tw.make_workload("S_mlp")
+    model = TorchModel(wl, "cuda", dtype=torch.float32)
+    L1, L2, grads = dregs_step(model)
+    torch.cuda.synchronize()
+    phi = model.proposal_params()
+    ref = [torch.zeros_like(p) for p in phi]
+    for b in range(wl.B):
+        lw = model.log_weights_bruteforce(b)
+        c = torch.exp(2 * lw - 2 * torch.logsumexp(lw, 0)).detach()
+        g = torch.autograd.grad((c * lw).sum(), phi, allow_unused=True)
+        ref = [r + (torch.zeros_like(r) if x is None else x) for r, x in zip(ref, g)]
+    for p, r in zip(phi, ref):
+        got = grads[p]
+        rel = (got - r).norm() / max(r.norm().item(), 1e-12)
+        assert rel < 2e-3, rel.item()

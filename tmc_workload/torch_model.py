@@ -67,8 +67,11 @@ class TorchModel:
                 h = torch.tanh(h)
         return h
 
-    def forward(self) -> Dict[str, list]:
-        """z, mu, logvar, logq, logobs per latent (ABI layout, fp32, contiguous) with autograd."""
+    def forward(self, stl: bool = False) -> Dict[str, list]:
+        """z, mu, logvar, logq, logobs per latent (ABI layout, fp32, contiguous) with autograd.
+
+        stl: "sticking the landing": log q is evaluated with the proposal parameters
+        detached, so its gradient reaches them only through the reparameterised samples z."""
         torch = self.torch
         cfg = self.cfg
         n, D, K = cfg.n, cfg.D, cfg.K
@@ -78,7 +81,12 @@ class TorchModel:
             for i in range(n):
                 sig = torch.exp(self.q_logsig[i])
                 z[i] = self.q_mu[i] + sig * self.eps[i]
-                lq[i] = (-0.5 * self.eps[i] ** 2 - self.q_logsig[i] - 0.5 * LOG2PI).sum(-1)
+                if stl:
+                    m_d, ls_d = self.q_mu[i].detach(), self.q_logsig[i].detach()
+                    e = (z[i] - m_d) * torch.exp(-ls_d)
+                    lq[i] = (-0.5 * e ** 2 - ls_d - 0.5 * LOG2PI).sum(-1)
+                else:
+                    lq[i] = (-0.5 * self.eps[i] ** 2 - self.q_logsig[i] - 0.5 * LOG2PI).sum(-1)
             for i in range(n):
                 if cfg.parent[i] < 0:
                     mu[i] = torch.zeros(B, 1, D[i], device=self.device)
@@ -123,6 +131,35 @@ class TorchModel:
                     gouts.append(grads[i][gk])
         torch.autograd.backward(outs, gouts)
 
+    def proposal_params(self):
+        """The recognition (proposal) parameters phi; everything else is generative (theta)."""
+        return list(self.q_mu) + list(self.q_logsig) if self.cfg.family == "mlp_chain" else []
+
+    def generative_params(self):
+        ph = {id(p) for p in self.proposal_params()}
+        return [p for p in self.params if id(p) not in ph]
+
+    def log_weights_bruteforce(self, b: int):
+        """log w for every index tuple of datapoint b (tiny instances only; test oracle of the
+        DReGs gradient): sum_i log p(z_i | z_pa) - log q(z_i) + log p(x | z), differentiable."""
+        import itertools
+        torch = self.torch
+        cfg = self.cfg
+        f = self.forward(stl=True)
+        n = cfg.n
+        out = []
+        for k in itertools.product(*[range(cfg.K) for _ in range(n)]):
+            s = 0.0
+            for i in range(n):
+                zi = f["z"][i][b, k[i]]
+                r = 0 if cfg.parent[i] < 0 else k[cfg.parent[i]]
+                mu, lv = f["mu"][i][b, r], f["logvar"][i][b, r]
+                s = s + (-0.5 * ((zi - mu) ** 2 * torch.exp(-lv) + lv + LOG2PI)).sum() - f["logq"][i][b, k[i]]
+                if f["logobs"][i] is not None:
+                    s = s + f["logobs"][i][b, k[i]]
+            out.append(s)
+        return torch.stack(out)
+
     def flat_grads(self):
         torch = self.torch
         return torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1) for p in self.params])
@@ -130,3 +167,55 @@ class TorchModel:
     def zero_grad(self):
         for p in self.params:
             p.grad = None
+
+
+def dregs_step(model: TorchModel, direction: int = 0, precision: int = 0):
+    """One TMC-DReGs gradient evaluation through libtmc, on the model's device.
+
+    Generative parameters theta get the usual TMC gradient of sum_b L1[b] (alpha = 1).  Recognition
+    parameters phi get the DReGs update sum_i w_i^2/(sum w)^2 dz_i/dphi dlog w_i/dz_i, computed from
+    the surrogate 1/2 (sum w^2/(sum w)^2) log sum w_hat^2: a second TMC run with squared weights
+    (factor_power = 2) gives L2 = log((1/prod K) sum w^2) and its input gradients, which are scaled
+    per datapoint by dlogp = 1/2 exp(L2 - 2 L1 - sum_i ln K_i) and pushed into phi through the
+    reparameterised samples only (STL form of log q: w_hat drops the direct phi term).
+    Returns (L1, L2, {param: grad}).
+    """
+    import paper_1806_08593_b200 as tmc
+    torch = model.torch
+    cfg = model.cfg
+    n = cfg.n
+    f = model.forward(stl=True)
+    inp = [dict(z=f["z"][i].detach(), mu=f["mu"][i].detach(), logvar=f["logvar"][i].detach(),
+                logq=f["logq"][i].detach(), logobs=None if f["logobs"][i] is None else f["logobs"][i].detach())
+           for i in range(n)]
+    B = inp[0]["z"].shape[0]
+    K = [cfg.K] * n
+
+    def outs_and_grads(grads):
+        outs, gouts = [], []
+        for k, gk in (("z", "dz"), ("mu", "dmu"), ("logvar", "dlogvar"), ("logq", "dlogq"), ("logobs", "dlogobs")):
+            for i, a in enumerate(f[k]):
+                if a is not None and a.requires_grad and grads[i].get(gk) is not None:
+                    outs.append(a)
+                    gouts.append(grads[i][gk])
+        return outs, gouts
+
+    g1 = tmc.Graph(cfg.parent, K, cfg.D, B, direction=direction, precision=precision, factor_power=1.0)
+    L1, gr1 = tmc.estimate(g1, inp)
+    g2 = tmc.Graph(cfg.parent, K, cfg.D, B, direction=direction, precision=precision, factor_power=2.0)
+    ws2 = tmc.alloc_workspace(g2, inp[0]["z"].device)
+    L2 = torch.empty(B, dtype=torch.float64, device=inp[0]["z"].device)
+    tmc.tmc_forward(g2, inp, L2, ws2)
+    lnK = sum(math.log(k) for k in K)
+    dlogp2 = 0.5 * torch.exp(L2 - 2.0 * L1 - lnK)
+    gr2 = tmc.alloc_grads(g2, inp[0]["z"].device)
+    tmc.tmc_backward(g2, inp, ws2, dlogp2, gr2)
+    theta, phi = model.generative_params(), model.proposal_params()
+    o1, go1 = outs_and_grads(gr1)
+    gt = torch.autograd.grad(o1, theta, go1, retain_graph=True, allow_unused=True)
+    o2, go2 = outs_and_grads(gr2)
+    gp = torch.autograd.grad(o2, phi, go2, allow_unused=True) if phi else []
+    res = {}
+    for p_, g_ in list(zip(theta, gt)) + list(zip(phi, gp)):
+        res[p_] = torch.zeros_like(p_) if g_ is None else g_
+    return L1, L2, res
