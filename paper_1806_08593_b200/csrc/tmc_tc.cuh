@@ -446,6 +446,7 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__
     float v = red[0];
     for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w]);
     red[16] = (v == -INFINITY) ? 0.f : v;
+    red[17] = (v == -INFINITY) ? 1.f : 0.f;   // no live column: every message of this datapoint is -inf
   }
   __syncthreads();
   const float cmax = red[16];
@@ -479,7 +480,9 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__
     double off = (double)cmax;
     if (a.off_cb) off += a.off_cb[b];
     if (a.off_rb) off += a.off_rb[b];
-    a.off_out[b] = off;
+    // All columns dead: the clamped biases above would leave a finite (-6e4-scale) LSE, so the
+    // offset carries the exact -inf (a sum of zero weights).
+    a.off_out[b] = red[17] != 0.f ? -INFINITY : off;
   }
 }
 
@@ -788,6 +791,9 @@ struct BwdArgs {
 };
 
 template <int D>
+#ifndef TMC_BWD_SPLIT
+#define TMC_BWD_SPLIT 1   // 1: S MMAs and gradient MMAs issued by two warps (see tc_bwd_kernel)
+#endif
 struct BGeo {
   static constexpr int TILE = Geo<D>::TILE;
   static constexpr int PART = Geo<D>::PART;
@@ -795,7 +801,7 @@ struct BGeo {
   static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
   static constexpr int SMW = 16;                               // softmax warps (4 per TMEM lane quarter)
   static constexpr int EW = 4;                                 // epilogue warps (1 per TMEM lane quarter)
-  static constexpr int THREADS = 32 * (SMW + EW + 2);
+  static constexpr int THREADS = 32 * (SMW + EW + 2 + TMC_BWD_SPLIT);
   static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 4 * 128 * 4 + 512;
 };
 
@@ -866,6 +872,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
   using G = BGeo<D>;
   constexpr int ST = G::ST, SMW = G::SMW, EW = G::EW;
   constexpr int W_PROD = SMW + EW, W_MMA = SMW + EW + 1;     // role warps take the highest ids
+  constexpr int W_MMAG = TMC_BWD_SPLIT ? W_MMA + 1 : W_MMA;  // gradient-MMA issuer (split mode)
   constexpr uint32_t IDESC_S = kIdescF16M128N128;
   constexpr bool PACKED = GT >= 4;
   constexpr uint32_t GN = PACKED ? 4 * D : 2 * D;            // N of the gradient MMA
@@ -962,7 +969,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
-  } else if (warp == W_MMA) {
+  } else if (warp == W_MMA || warp == W_MMAG) {
     TMC_PROF_T0(_tr1);
     {   // ---------------- MMA issuer (whole warp, one elected lane issues)
 #if defined(TMC_INSTRUMENT) && TMC_MMA_PROF == 2
@@ -1003,6 +1010,25 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
         mma_commit(&s_empty[as]);
         TMC_PROF_END_M(16, _tc);
       };
+      // Split mode: a second warp issues the gradient GEMMs, so the S issue stream never stalls on
+      // the P~ hand-off of the previous tile (each thread's tcgen05.commit tracks its own MMAs; the
+      // gradient MMA of tile j is issued after p_full(j), which implies S(j) completed, so its
+      // commit may free both the S buffer and the streamed tile).
+      if (TMC_BWD_SPLIT && warp == W_MMAG) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+          TMC_BWD_UNIT();
+          if (!olive(a, b, mt)) continue;
+          int jj = 0;
+          for (int j = 0; j < a.t_tiles; ++j) {
+            if (!tlive(a, b, j)) continue;
+            grad(a, t, jj == 0);
+            ++jj;
+            ++t;
+          }
+          mma_commit(&g_full[ua % GB]);
+          ++ua;
+        }
+      } else
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         TMC_BWD_UNIT();
         if (!olive(a, b, mt)) continue;
@@ -1038,12 +1064,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
           TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
           TMC_PROF_END_M(18, _tc2);
-          if (jj > 0) grad(a, t - 1, jj == 1);
+          if (!TMC_BWD_SPLIT && jj > 0) grad(a, t - 1, jj == 1);
           ++jj;
           ++t;
         }
-        if (jj > 0) grad(a, t - 1, jj == 1);
-        mma_commit(&g_full[ua % GB]);
+        if (!TMC_BWD_SPLIT) {
+          if (jj > 0) grad(a, t - 1, jj == 1);
+          mma_commit(&g_full[ua % GB]);
+        }
         mma_commit(o_empty);
         ++ua;
       }

@@ -298,3 +298,43 @@ def test_dregs_gradient_matches_bruteforce(torch_cuda):
         got = grads[p]
         rel = (got - r).norm() / max(r.norm().item(), 1e-12)
         assert rel < 2e-3, rel.item()
+
+
+_NAN_PROBE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import tmc_workload as tw, paper_1806_08593_b200 as tmc
+wl = tw.make_workload({name!r}, B=4, K={K})
+if {mode!r} == "nan":
+    wl.z[1][2, 7, 0] = np.nan             # one non-finite sample in datapoint 2
+else:
+    wl.logobs[len(wl.parent) - 1][2, :] = -np.inf   # datapoint 2: every weight exactly 0
+t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+inp = [dict(z=t(wl.z[i]), mu=t(wl.mu[i]), logvar=t(wl.logvar[i]), logq=t(wl.logq[i]), logobs=t(wl.logobs[i]))
+       for i in range(len(wl.parent))]
+g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction={direction})
+logp, gr = tmc.estimate(g, inp)
+torch.cuda.synchronize()
+np.save({out!r}, np.stack([logp.cpu().numpy()] + [gr[i]["dz"].cpu().numpy().reshape(4, -1).sum(1) for i in range(len(wl.parent))]))
+"""
+
+
+@pytest.mark.parametrize("mode", ["nan", "neginf"])
+@pytest.mark.parametrize("name,K,direction", [("C3", 300, 2), ("C3", 300, 1), ("C4", 160, 0)])
+def test_nonfinite_input_terminates_and_stays_local(torch_cuda, name, K, direction, mode, tmp_path):
+    """A NaN input, or a datapoint whose weights are all exactly 0, must neither hang a pipelined
+    kernel nor leak into other datapoints: run in a child process with a deadline; datapoints
+    0, 1, 3 must still match the oracle (and an all-zero datapoint gives logp = -inf)."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "r.npy")
+    code = _NAN_PROBE.format(root=root, name=name, K=K, direction=direction, out=out, mode=mode)
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=180)
+    r = np.load(out)
+    clean = tw.make_workload(name, B=4, K=K)
+    ref = oracle.estimate_workload(clean, grads=False)
+    for b in (0, 1, 3):
+        assert abs(r[0, b] - ref["logp"][b]) <= LOGP_TOL, (b, r[0, b], ref["logp"][b])
+    if mode == "neginf":
+        assert r[0, 2] == -np.inf
+        assert np.isfinite(r[1:, 2]).all()     # zero weight => zero gradient, not NaN
