@@ -147,6 +147,26 @@ tmc_status tmc_backward(const tmc_graph *g, const tmc_latent_in *in, const float
 tmc_status tmc_estimate(const tmc_graph *g, const tmc_latent_in *in, double *logp, const double *dlogp,
                         tmc_latent_grad *out, void *ws, size_t ws_bytes, tmc_stream_t stream);
 
+/* Streamed estimate from HOST inputs (the end-to-end path of a caller whose samples live in
+ * host memory).  Datapoints are independent problems, so the batch is cut into
+ * chunks of `chunk` datapoints: chunk c+1's inputs are copied host->device on an internal
+ * copy stream (one per device, created on first use) into one of two staging slots of `ws`
+ * while chunk c runs tmc_estimate on `stream`; PCIe transfer and kernels overlap.
+ *   in         HOST array of n tmc_latent_in whose buffers are HOST memory, same layouts as
+ *              tmc_latent_in (page-locked for the overlap; pageable memory works, serialised).
+ *   logp_host  HOST fp64 [B]; written by the time `stream` passes the call's last operation
+ *              (page-locked for an asynchronous copy).
+ *   dlogp_host HOST fp64 [B] or NULL (= all ones).
+ *   out        DEVICE gradients in the full-batch layout of tmc_latent_grad, or NULL for
+ *              logp only.
+ *   ws         DEVICE workspace of tmc_estimate_host_workspace_size(g, chunk) bytes: two
+ *              input staging slots + the tmc_estimate workspace of one chunk.
+ * The host buffers must stay valid and unmodified until `stream` completes the call's work. */
+size_t tmc_estimate_host_workspace_size(const tmc_graph *g, int32_t chunk);
+tmc_status tmc_estimate_host(const tmc_graph *g, const tmc_latent_in *in, double *logp_host,
+                             const double *dlogp_host, tmc_latent_grad *out, int32_t chunk, void *ws,
+                             size_t ws_bytes, tmc_stream_t stream);
+
 /* Thread-local message describing the last non-OK status on this thread. */
 const char *tmc_last_error(void);
 

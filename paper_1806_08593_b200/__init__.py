@@ -24,6 +24,7 @@ STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_
           -7: "TMC_ERR_CUDA", -8: "TMC_ERR_NONFINITE"}
 
 EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate",
+           "tmc_estimate_host_workspace_size", "tmc_estimate_host",
            "tmc_last_error", "tmc_version", "tmc_launch_count"]
 
 
@@ -68,7 +69,11 @@ def load_library(path: str = LIB_PATH):
                                      ctypes.POINTER(tmc_latent_grad), P, P]
         lib.tmc_estimate.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P,
                                      ctypes.POINTER(tmc_latent_grad), P, ctypes.c_size_t, P]
-        for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate"):
+        lib.tmc_estimate_host_workspace_size.restype = ctypes.c_size_t
+        lib.tmc_estimate_host_workspace_size.argtypes = [G, ctypes.c_int32]
+        lib.tmc_estimate_host.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, ctypes.POINTER(tmc_latent_grad),
+                                          ctypes.c_int32, P, ctypes.c_size_t, P]
+        for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate", "tmc_estimate_host"):
             getattr(lib, f).restype = ctypes.c_int
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
@@ -181,6 +186,21 @@ def tmc_estimate(graph: Graph, inputs: List[Dict], logp, dlogp, grads: Optional[
     _check(load_library().tmc_estimate(graph.ref(), _inputs(inputs), _dp(logp), _dp(dlogp),
                                        _grads(grads, graph.n), _dp(ws), ws.numel() * ws.element_size(),
                                        _stream(stream)))
+
+
+def tmc_estimate_host_workspace_size(graph: Graph, chunk: int) -> int:
+    n = load_library().tmc_estimate_host_workspace_size(graph.ref(), int(chunk))
+    if n == 0:
+        raise TmcError(-2, load_library().tmc_last_error().decode())
+    return n
+
+
+def tmc_estimate_host(graph: Graph, host_inputs: List[Dict], logp_host, dlogp_host, grads: Optional[List[Dict]],
+                      chunk: int, ws, stream=None) -> None:
+    """host_inputs / logp_host / dlogp_host: CPU tensors (pinned for overlap); grads: device tensors."""
+    _check(load_library().tmc_estimate_host(graph.ref(), _inputs(host_inputs), _dp(logp_host), _dp(dlogp_host),
+                                            None if grads is None else _grads(grads, graph.n), int(chunk),
+                                            _dp(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def tmc_last_error() -> str:

@@ -501,6 +501,65 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
 }  // namespace
 }  // namespace tmc
 
+
+// ============================================================ host-input streamed estimate (e2e)
+// tmc_estimate_host: the batch is cut into chunks of datapoints (independent problems),
+// chunk c+1's inputs are copied host->device on an internal copy stream into one of two staging
+// slots while chunk c runs on the caller's stream, so PCIe transfer and kernels overlap.
+namespace tmc {
+namespace {
+
+struct HostPipe {            // per device: the copy stream and slot events (created once, never freed)
+  cudaStream_t copy = nullptr;
+  cudaEvent_t start = nullptr, copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+};
+
+tmc_status host_pipe(HostPipe*& hp) {
+  static std::mutex mu;
+  static HostPipe pipes[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(TMC_ERR_CUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(mu);
+  HostPipe& h = pipes[dev];
+  if (!h.copy) {
+    if (cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking) != cudaSuccess) return fail(TMC_ERR_CUDA, "copy stream");
+    cudaEvent_t* evs[5] = {&h.start, &h.copied[0], &h.copied[1], &h.done[0], &h.done[1]};
+    for (cudaEvent_t* e : evs)
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail(TMC_ERR_CUDA, "event");
+  }
+  hp = &h;
+  return TMC_OK;
+}
+
+// Floats one datapoint's inputs take, per latent field, in staging order (z, mu, logvar, logq, logobs).
+struct StageLayout {
+  std::vector<size_t> off[5];   // [field][latent] byte offset inside a slot for chunk datapoints
+  size_t slot_bytes = 0, dlogp_off = 0, ws_off = 0, total = 0;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+void stage_layout(const tmc_graph* g, int chunk, size_t ws_chunk, StageLayout& L) {
+  size_t cur = 0;
+  for (int f = 0; f < 5; ++f) L.off[f].assign(g->n, 0);
+  for (int i = 0; i < g->n; ++i) {
+    const size_t K = g->K[i], D = g->D[i], Kp = g->parent[i] < 0 ? 1 : g->K[g->parent[i]];
+    const size_t per[5] = {K * D, Kp * D, Kp * D, K, K};
+    for (int f = 0; f < 5; ++f) {
+      L.off[f][i] = cur;
+      cur = align256(cur + (size_t)chunk * per[f] * sizeof(float));
+    }
+  }
+  L.dlogp_off = cur;
+  cur = align256(cur + (size_t)chunk * sizeof(double));
+  L.slot_bytes = cur;
+  L.ws_off = align256(2 * L.slot_bytes + (size_t)chunk * sizeof(double) * 2);
+  L.total = L.ws_off + ws_chunk;
+}
+
+}  // namespace
+}  // namespace tmc
+
 // ====================================================================================== C ABI
 using namespace tmc;
 
@@ -578,6 +637,100 @@ tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* log
   tmc_status st = tmc_forward(g, in, nullptr, logp, ws, ws_bytes, stream);
   if (st != TMC_OK) return st;
   return tmc_backward(g, in, nullptr, ws, ws_bytes, dlogp, out, nullptr, stream);
+}
+
+
+size_t tmc_estimate_host_workspace_size(const tmc_graph* g, int32_t chunk) {
+  if (!g || chunk <= 0) return 0;
+  tmc_graph gc = *g;
+  gc.B = std::min<int32_t>(chunk, std::max<int32_t>(g->B, 1));
+  Plan p;
+  if (make_plan(&gc, false, p) != TMC_OK) return 0;
+  StageLayout L;
+  stage_layout(g, gc.B, p.total, L);
+  return L.total;
+}
+
+tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double* logp_host, const double* dlogp_host,
+                             tmc_latent_grad* out, int32_t chunk, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = make_plan(g, false, p);
+    if (st != TMC_OK) return st;
+    if (chunk <= 0) return fail(TMC_ERR_INVALID_ARG, "chunk must be > 0");
+    if (!in || (!logp_host && p.B > 0)) return fail(TMC_ERR_INVALID_ARG, "tmc_estimate_host: NULL input/logp");
+    for (int i = 0; i < p.n; ++i)
+      if (!in[i].z || !in[i].mu || !in[i].logvar || !in[i].logq) return fail(TMC_ERR_INVALID_ARG, "NULL input buffer");
+    if (p.B == 0) return TMC_OK;
+    const int cb = std::min<int>(chunk, p.B);
+    const size_t need = tmc_estimate_host_workspace_size(g, cb);
+    if (!ws || ws_bytes < need) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    if ((st = check_device()) != TMC_OK) return st;
+    tmc_graph gc = *g;
+    gc.B = cb;
+    Plan pc;
+    if ((st = make_plan(&gc, false, pc)) != TMC_OK) return st;
+    StageLayout L;
+    stage_layout(g, cb, pc.total, L);
+    HostPipe* hp = nullptr;
+    if ((st = host_pipe(hp)) != TMC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    double* logp_dev = reinterpret_cast<double*>(w + 2 * L.slot_bytes);
+    // the copy stream may overwrite the staging slots only after earlier work on `stream`
+    cudaEventRecord(hp->start, s);
+    cudaStreamWaitEvent(hp->copy, hp->start, 0);
+    const int nchunks = (p.B + cb - 1) / cb;
+    std::vector<tmc_latent_in> cin(p.n);
+    std::vector<tmc_latent_grad> cout(p.n);
+    for (int c = 0; c < nchunks; ++c) {
+      const int b0 = c * cb, bc = std::min(cb, p.B - b0), sl = c & 1;
+      uint8_t* slot = w + (size_t)sl * L.slot_bytes;
+      if (c >= 2) cudaStreamWaitEvent(hp->copy, hp->done[sl], 0);
+      for (int i = 0; i < p.n; ++i) {
+        const size_t K = p.K[i], D = p.D[i], Kp = p.Kp[i];
+        const size_t per[5] = {K * D, Kp * D, Kp * D, K, K};
+        const float* src[5] = {in[i].z, in[i].mu, in[i].logvar, in[i].logq, in[i].logobs};
+        float* dst[5];
+        for (int f = 0; f < 5; ++f) {
+          dst[f] = reinterpret_cast<float*>(slot + L.off[f][i]);
+          if (src[f] && cudaMemcpyAsync(dst[f], src[f] + (size_t)b0 * per[f], (size_t)bc * per[f] * sizeof(float),
+                                        cudaMemcpyHostToDevice, hp->copy) != cudaSuccess)
+            return fail(TMC_ERR_CUDA, "host->device copy failed");
+        }
+        cin[i] = tmc_latent_in{dst[0], dst[1], dst[2], dst[3], in[i].logobs ? dst[4] : nullptr};
+        tmc_latent_grad o{};
+        if (out) {
+          const tmc_latent_grad& O = out[i];
+          o.dz = O.dz ? O.dz + (size_t)b0 * K * D : nullptr;
+          o.dmu = O.dmu ? O.dmu + (size_t)b0 * Kp * D : nullptr;
+          o.dlogvar = O.dlogvar ? O.dlogvar + (size_t)b0 * Kp * D : nullptr;
+          o.dlogq = O.dlogq ? O.dlogq + (size_t)b0 * K : nullptr;
+          o.dlogobs = O.dlogobs ? O.dlogobs + (size_t)b0 * K : nullptr;
+          o.pair_marginal = O.pair_marginal ? O.pair_marginal + (size_t)b0 * K * Kp : nullptr;
+        }
+        cout[i] = o;
+      }
+      double* dl = nullptr;
+      if (dlogp_host) {
+        dl = reinterpret_cast<double*>(slot + L.dlogp_off);
+        if (cudaMemcpyAsync(dl, dlogp_host + b0, (size_t)bc * sizeof(double), cudaMemcpyHostToDevice, hp->copy) != cudaSuccess)
+          return fail(TMC_ERR_CUDA, "host->device copy failed");
+      }
+      cudaEventRecord(hp->copied[sl], hp->copy);
+      cudaStreamWaitEvent(s, hp->copied[sl], 0);
+      gc.B = bc;
+      st = out ? tmc_estimate(&gc, cin.data(), logp_dev + b0 % (2 * cb), dl, cout.data(), w + L.ws_off, pc.total, stream)
+               : tmc_forward(&gc, cin.data(), nullptr, logp_dev + b0 % (2 * cb), w + L.ws_off, pc.total, stream);
+      if (st != TMC_OK) return st;
+      if (cudaMemcpyAsync(logp_host + b0, logp_dev + b0 % (2 * cb), (size_t)bc * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return fail(TMC_ERR_CUDA, "device->host copy failed");
+      cudaEventRecord(hp->done[sl], s);
+    }
+    return launch_check("tmc_estimate_host");
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
 }
 
 const char* tmc_last_error(void) { return g_err.c_str(); }
