@@ -147,6 +147,27 @@ tmc_status tmc_backward(const tmc_graph *g, const tmc_latent_in *in, const float
 tmc_status tmc_estimate(const tmc_graph *g, const tmc_latent_in *in, double *logp, const double *dlogp,
                         tmc_latent_grad *out, void *ws, size_t ws_bytes, tmc_stream_t stream);
 
+/* Shared-root trees sharded over processes (the star graph of P:334-346: a global latent theta
+ * with K_theta samples shared by N data points, each with its own latent z_i).  Each shard holds
+ * the root and a subset of its children (subtrees); the root's incoming messages are additive in
+ * the log domain, so the TMC estimate needs ONE exchange:
+ *   1. tmc_forward_children on every shard: the forward pass of every latent below the root;
+ *      root_msg (DEVICE fp64 [B][K_root+1]) receives, for datapoint b, the sum over this shard's
+ *      root children j of msg_{j->root}[b][r] as fp32 residuals summed in fp64 (r < K_root) and
+ *      the sum of their fp64 offsets (entry K_root).  A shard without children writes zeros.
+ *   2. the caller sums root_msg over shards (e.g. ncclAllReduce SUM, fp64).
+ *   3. tmc_forward_root on every shard with the summed root_msg: h_root = u_root + sum, the
+ *      root's elimination and logp (identical on every shard).
+ *   4. tmc_backward as usual: gradients of this shard's latents under the global root marginal.
+ *      The root's own gradients (dz/dmu/dlogvar/dlogq/dlogobs of the root) are computed on every
+ *      shard identically; count them once.
+ * Requirements: exactly one root, direction = TMC_DIR_UP (explicitly: a shard holding one child
+ * is a chain), the same workspace for steps 1, 3 and 4 on the same stream. */
+tmc_status tmc_forward_children(const tmc_graph *g, const tmc_latent_in *in, double *root_msg, void *ws,
+                                size_t ws_bytes, tmc_stream_t stream);
+tmc_status tmc_forward_root(const tmc_graph *g, const tmc_latent_in *in, const double *root_msg_total,
+                            double *logp, void *ws, size_t ws_bytes, tmc_stream_t stream);
+
 /* Streamed estimate from HOST inputs (the end-to-end path of a caller whose samples live in
  * host memory).  Datapoints are independent problems, so the batch is cut into
  * chunks of `chunk` datapoints: chunk c+1's inputs are copied host->device on an internal

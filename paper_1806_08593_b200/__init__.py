@@ -24,6 +24,7 @@ STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_
           -7: "TMC_ERR_CUDA", -8: "TMC_ERR_NONFINITE"}
 
 EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate",
+           "tmc_forward_children", "tmc_forward_root",
            "tmc_estimate_host_workspace_size", "tmc_estimate_host",
            "tmc_last_error", "tmc_version", "tmc_launch_count"]
 
@@ -73,7 +74,10 @@ def load_library(path: str = LIB_PATH):
         lib.tmc_estimate_host_workspace_size.argtypes = [G, ctypes.c_int32]
         lib.tmc_estimate_host.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, ctypes.POINTER(tmc_latent_grad),
                                           ctypes.c_int32, P, ctypes.c_size_t, P]
-        for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate", "tmc_estimate_host"):
+        lib.tmc_forward_children.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, ctypes.c_size_t, P]
+        lib.tmc_forward_root.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, P, ctypes.c_size_t, P]
+        for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate", "tmc_estimate_host",
+                  "tmc_forward_children", "tmc_forward_root"):
             getattr(lib, f).restype = ctypes.c_int
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
@@ -186,6 +190,18 @@ def tmc_estimate(graph: Graph, inputs: List[Dict], logp, dlogp, grads: Optional[
     _check(load_library().tmc_estimate(graph.ref(), _inputs(inputs), _dp(logp), _dp(dlogp),
                                        _grads(grads, graph.n), _dp(ws), ws.numel() * ws.element_size(),
                                        _stream(stream)))
+
+
+def tmc_forward_children(graph: Graph, inputs: List[Dict], root_msg, ws, stream=None) -> None:
+    """Shared-root exchange step 1: root_msg (fp64 [B][K_root+1]) = this shard's child messages."""
+    _check(load_library().tmc_forward_children(graph.ref(), _inputs(inputs), _dp(root_msg), _dp(ws),
+                                               ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def tmc_forward_root(graph: Graph, inputs: List[Dict], root_msg_total, logp, ws, stream=None) -> None:
+    """Shared-root exchange step 3: the root's elimination from the shard-summed root_msg."""
+    _check(load_library().tmc_forward_root(graph.ref(), _inputs(inputs), _dp(root_msg_total), _dp(logp),
+                                           _dp(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def tmc_estimate_host_workspace_size(graph: Graph, chunk: int) -> int:

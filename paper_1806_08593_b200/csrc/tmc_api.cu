@@ -182,6 +182,7 @@ void launch_pass_t(const PassArgs& a, cudaStream_t s) {
 template <bool ZR, int MODE>
 void launch_pass_m(const PassArgs& a, bool dense, cudaStream_t s) {
   if (dense) return launch_pass_t<ZR, MODE, true, 1>(a, s);
+  if (a.D <= 4) return launch_pass_t<ZR, MODE, false, 0>(a, s);
   if (a.D <= 32) return launch_pass_t<ZR, MODE, false, 1>(a, s);
   if (a.D <= 64) return launch_pass_t<ZR, MODE, false, 2>(a, s);
   if (a.D <= 128) return launch_pass_t<ZR, MODE, false, 4>(a, s);
@@ -209,6 +210,54 @@ void launch_pass(const PassArgs& a, bool zrows, int mode, bool dense, cudaStream
   }
 }
 
+template <bool ZR, int MODE, bool DENSE, int MAXDL>
+void launch_pass_batch_t(const PassArgs* as, int ne, cudaStream_t s) {
+  auto kern = simt::pass_batch_kernel<ZR, MODE, DENSE, MAXDL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  for (int e0 = 0; e0 < ne; e0 += simt::kMaxPassBatch) {
+    simt::PassBatch pb{};
+    const int n = std::min(simt::kMaxPassBatch, ne - e0);
+    int maxNO = 0, maxD = 1;
+    for (int k = 0; k < n; ++k) {
+      pb.e[k] = as[e0 + k];
+      maxNO = std::max(maxNO, MODE != 2 ? pb.e[k].R : pb.e[k].C);
+      maxD = std::max(maxD, pb.e[k].D);
+    }
+    dim3 grid((maxNO + simt::kOPC - 1) / simt::kOPC, as[0].B, n);
+    kern<<<grid, simt::kThreads, simt::pass_smem_bytes(maxD, DENSE), s>>>(pb);
+    TMC_COUNT_LAUNCH();
+  }
+}
+
+template <int MODE, bool DENSE, int MAXDL>
+void launch_pass_batch_c(const std::vector<PassArgs>& v, cudaStream_t s) {
+  if (!v.empty()) launch_pass_batch_t<false, MODE, DENSE, MAXDL>(v.data(), (int)v.size(), s);
+}
+
+template <int MODE>
+void launch_pass_batch_m(const std::vector<PassArgs>& as, bool dense, cudaStream_t s) {
+  if (dense) return launch_pass_batch_c<MODE, true, 1>(as, s);
+  std::vector<PassArgs> cls[5];
+  for (const PassArgs& a : as) cls[a.D <= 4 ? 4 : a.D <= 32 ? 0 : a.D <= 64 ? 1 : a.D <= 128 ? 2 : 3].push_back(a);
+  launch_pass_batch_c<MODE, false, 0>(cls[4], s);
+  launch_pass_batch_c<MODE, false, 1>(cls[0], s);
+  launch_pass_batch_c<MODE, false, 2>(cls[1], s);
+  launch_pass_batch_c<MODE, false, 4>(cls[2], s);
+  launch_pass_batch_c<MODE, false, 8>(cls[3], s);
+}
+
+// SIMT passes of the independent edges of one UP level (rows = parent samples), batched.
+void launch_pass_batch(const std::vector<PassArgs>& as, int mode, bool dense, cudaStream_t s) {
+  if (as.empty() || as[0].B == 0) return;
+  if (mode == 0) launch_pass_batch_m<0>(as, dense, s);
+  else if (mode == 1) launch_pass_batch_m<1>(as, dense, s);
+  else launch_pass_batch_m<2>(as, dense, s);
+}
+
 // Common PassArgs of edge i (inputs, geometry, forward state).
 PassArgs edge_args(const Plan& p, int i, const tmc_latent_in* in, const float* const* dense, void* ws) {
   PassArgs a{};
@@ -230,8 +279,10 @@ PassArgs edge_args(const Plan& p, int i, const tmc_latent_in* in, const float* c
     a.off_rb = at<double>(ws, p.uoff[i]);
     a.lnC = par < 0 ? 0.f : std::log((float)p.Kp[i]);
   } else {
-    a.cb = at<float>(ws, e.h);
-    a.off_cb = at<double>(ws, e.hoff);
+    // h_i = u_i + child messages; a non-root leaf's h is its unary (no copy is built)
+    const bool leaf = p.children[i].empty() && p.parent[i] >= 0;   // roots keep h (shared-root exchange)
+    a.cb = leaf ? at<float>(ws, p.u[i]) : at<float>(ws, e.h);
+    a.off_cb = leaf ? at<double>(ws, p.uoff[i]) : at<double>(ws, e.hoff);
     a.rb = nullptr;
     a.off_rb = nullptr;
     a.lnC = std::log((float)p.K[i]);
@@ -284,10 +335,16 @@ tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* 
 }
 
 // ------------------------------------------------------------------------------------ forward
+// phase: 0 = the whole forward; 1 = every latent below the (single) root, then the root's child
+// messages summed into xout [B][K_root+1] (fp64 residual sums, then the offset sum); 2 = the root's
+// elimination from h_root = u_root + xin (xin = the sum of phase-1 outputs over the shards of the
+// root's children) and logp.  Phases 1 + 2 on one shard equal phase 0.
 tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* const* dense, double* logp,
-                        void* ws, cudaStream_t s) {
+                        void* ws, cudaStream_t s, int phase = 0, double* xout = nullptr,
+                        const double* xin = nullptr) {
   if (p.B == 0) return TMC_OK;
   // unary prep (all latents)
+  if (phase != 2)
   for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
     UnaryBatch ub{};
     ub.B = p.B;
@@ -330,7 +387,9 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       for (int c : p.children[i]) height[i] = std::max(height[i], height[c] + 1);
       maxh = std::max(maxh, height[i]);
     }
+    const int root0 = p.roots.empty() ? 0 : p.roots[0];
     for (int h = 0; h <= maxh; ++h) {
+      if ((phase == 1 && h == maxh) || (phase == 2 && h < maxh)) continue;
       std::vector<int> level;
       for (int i = p.n - 1; i >= 0; --i)
         if (height[i] == h) level.push_back(i);
@@ -338,6 +397,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       std::vector<const TcLatentBuf*> tcT;
       int tcD = 0;
       std::vector<PrepJob> prepJ;
+      std::vector<PassArgs> simtA;
       auto flush_tc = [&]() {
         if (!tcA.empty()) {
           g_launches.fetch_add(tc_prep_batch(prepJ.data(), (int)prepJ.size(), p.B, ws, s));
@@ -351,6 +411,13 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
         // h_i = u_i + sum of child messages
         const std::vector<int>& ch = p.children[i];
         int done = 0;
+        if (phase == 2 && i == root0) {
+          simt::hroot_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(
+              at<float>(ws, p.u[i]), at<double>(ws, p.uoff[i]), xin, p.K[i], at<float>(ws, p.e[i].h),
+              at<double>(ws, p.e[i].hoff));
+          TMC_COUNT_LAUNCH();
+          done = (int)ch.size();
+        } else if (!ch.empty() || p.parent[i] < 0)
         do {
           HBuild hb{};
           hb.B = p.B; hb.K = p.K[i];
@@ -374,12 +441,31 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
           tcD = p.D[i];
           tcA.push_back(a);
           tcT.push_back(&p.tc[i]);
-          prepJ.push_back(PrepJob{p.K[i], p.Kp[i], p.D[i], &in[i], &p.tc[i], at<float>(ws, p.e[i].h), p.K[i], 1, p.alpha});
+          prepJ.push_back(PrepJob{p.K[i], p.Kp[i], p.D[i], &in[i], &p.tc[i], a.cb, p.K[i], 1, p.alpha});
         } else {
-          launch_pass(a, /*zrows=*/false, 0, dense != nullptr, s);
+          simtA.push_back(a);
         }
       }
       flush_tc();
+      launch_pass_batch(simtA, 0, dense != nullptr, s);
+    }
+    if (phase == 1) {
+      // the root's incoming messages, summed over this shard's children (fp64)
+      const std::vector<int>& ch = p.children[root0];
+      for (int done = 0; done < (int)ch.size() || done == 0;) {
+        HBuild hb{};
+        hb.B = p.B; hb.K = p.K[root0];
+        hb.nchild = std::min<int>(kMaxChildren, (int)ch.size() - done);
+        for (int j = 0; j < hb.nchild; ++j) {
+          hb.msg[j] = at<float>(ws, p.e[ch[done + j]].out);
+          hb.moff[j] = at<double>(ws, p.e[ch[done + j]].off);
+        }
+        simt::xmsg_kernel<<<dim3((p.K[root0] + 1 + 255) / 256, p.B), 256, 0, s>>>(hb, xout, done == 0);
+        TMC_COUNT_LAUNCH();
+        done += std::max(hb.nchild, 1);
+        if (done >= (int)ch.size()) break;
+      }
+      return launch_check("tmc_forward_children");
     }
     RootList rl{};
     rl.B = p.B;
@@ -439,7 +525,7 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       maxd = std::max(maxd, depth[i]);
     }
     for (int dl = 0; dl <= maxd; ++dl) {
-      std::vector<PassArgs> rowA, colA;
+      std::vector<PassArgs> rowA, colA, simtRow, simtCol;
       std::vector<const TcLatentBuf*> tcT;
       std::vector<int> tcI;
       for (int i = 0; i < p.n; ++i) {
@@ -463,10 +549,12 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
           tcT.push_back(&p.tc[i]);
           tcI.push_back(i);
         } else {
-          launch_pass(a, false, 1, dense != nullptr, s);
-          launch_pass(c, false, 2, dense != nullptr, s);
+          simtRow.push_back(a);
+          simtCol.push_back(c);
         }
       }
+      launch_pass_batch(simtRow, 1, dense != nullptr, s);
+      launch_pass_batch(simtCol, 2, dense != nullptr, s);
       // batched tensor-core passes, grouped by D (row-owner passes of the level, then column owners)
       for (int Dv : {32, 64}) {
         std::vector<PassArgs> ra, ca;
@@ -639,6 +727,47 @@ tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* log
   return tmc_backward(g, in, nullptr, ws, ws_bytes, dlogp, out, nullptr, stream);
 }
 
+
+namespace {
+tmc_status exchange_plan(const tmc_graph* g, const tmc_latent_in* in, void* ws, size_t ws_bytes, Plan& p) {
+  tmc_status st = make_plan(g, false, p);
+  if (st != TMC_OK) return st;
+  if (p.dir != TMC_DIR_UP) return fail(TMC_ERR_GRAPH, "shared-root exchange needs direction = TMC_DIR_UP");
+  if (p.roots.size() != 1) return fail(TMC_ERR_GRAPH, "shared-root exchange needs exactly one root");
+  if ((st = check_inputs(p, in, nullptr)) != TMC_OK) return st;
+  if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+  return check_device();
+}
+}  // namespace
+
+tmc_status tmc_forward_children(const tmc_graph* g, const tmc_latent_in* in, double* root_msg, void* ws,
+                                size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = exchange_plan(g, in, ws, ws_bytes, p);
+    if (st != TMC_OK) return st;
+    if (!root_msg && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "root_msg is NULL");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (g->flags & TMC_FLAG_VALIDATE)
+      if ((st = validate_inputs(p, in, nullptr, ws, s)) != TMC_OK) return st;
+    return forward_impl(p, in, nullptr, nullptr, ws, s, 1, root_msg, nullptr);
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_forward_root(const tmc_graph* g, const tmc_latent_in* in, const double* root_msg_total, double* logp,
+                            void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = exchange_plan(g, in, ws, ws_bytes, p);
+    if (st != TMC_OK) return st;
+    if ((!root_msg_total || !logp) && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "root_msg_total / logp is NULL");
+    return forward_impl(p, in, nullptr, logp, ws, reinterpret_cast<cudaStream_t>(stream), 2, nullptr, root_msg_total);
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
 
 size_t tmc_estimate_host_workspace_size(const tmc_graph* g, int32_t chunk) {
   if (!g || chunk <= 0) return 0;

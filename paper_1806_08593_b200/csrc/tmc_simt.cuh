@@ -59,7 +59,7 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2
 }
 
 template <bool ZROWS, int MODE, bool DENSE, int MAXDL>
-__global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
+__device__ __forceinline__ void pass_body(const PassArgs& a) {
   constexpr bool OWNER_ROW = (MODE != 2);
   constexpr bool OWNER_Z = ZROWS ? (MODE != 2) : (MODE == 2);   // owner vectors are z-side
   const int b = blockIdx.y;
@@ -161,14 +161,18 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
     os1[ol] = s1;
   }
 
-  // per-lane state
+  // per-lane state.  SMALL (MAXDL == 0, D <= 4): each lane accumulates the owner-side Gaussian
+  // gradient sums over its own streamed entries in phase 1 (warp-reduced in the epilogue) instead
+  // of the lanes-over-dimensions phase 2, which would leave 31 of 32 lanes idle.
+  constexpr bool SMALL = (MAXDL == 0);
+  constexpr int NDL = SMALL ? 4 : MAXDL;
   float lm[kOPW], ls[kOPW], ptot[kOPW];
-  float acc0[kOPW][MAXDL], acc1[kOPW][MAXDL];
+  float acc0[kOPW][NDL], acc1[kOPW][NDL];
 #pragma unroll
   for (int j = 0; j < kOPW; ++j) {
     lm[j] = -INFINITY; ls[j] = 0.f; ptot[j] = 0.f;
 #pragma unroll
-    for (int q = 0; q < MAXDL; ++q) { acc0[j][q] = 0.f; acc1[j][q] = 0.f; }
+    for (int q = 0; q < NDL; ++q) { acc0[j][q] = 0.f; acc1[j][q] = 0.f; }
   }
 
   for (int s0 = 0; s0 < NS; s0 += kTC) {
@@ -235,14 +239,30 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
           float cbv = MODE == 1 ? ss0[sl] : os0[ol];
           float P = 0.f;
           if (wr != 0.f && el > -INFINITY) P = wr * __expf(g + cbv - cbmax - el);
-          pbuf[(warp * kOPW + j) * kTC + sl] = P;
+          if constexpr (SMALL && !DENSE) {
+            const float* zv = OWNER_Z ? ov0 + ol * SD : sv0 + sl * SD;
+            const float* mv = OWNER_Z ? sv0 + sl * SD : ov0 + ol * SD;
+#pragma unroll
+            for (int q = 0; q < NDL; ++q) {
+              if (q >= D) break;
+              if (OWNER_Z) {     // dz_o,q += P (mu_s,q - z_o,q) lam_s,q
+                acc0[j][q] = fmaf(P * (mv[q] - zv[q]), sv1[sl * SD + q], acc0[j][q]);
+              } else {           // sum_s P (z_s,q - mu_o,q) and sum_s P (z_s,q - mu_o,q)^2
+                const float df = zv[q] - mv[q], pd = P * df;
+                acc0[j][q] += pd;
+                acc1[j][q] = fmaf(pd, df, acc1[j][q]);
+              }
+            }
+          } else {
+            pbuf[(warp * kOPW + j) * kTC + sl] = P;
+          }
           ptot[j] += P;
           if (MODE == 1 && a.pair) a.pair[((int64_t)b * a.Kz + ai) * a.Kp + pi] = a.alpha * P;
         }
       }
     }
     // ---- phase 2: lanes over dimensions (owner-side Gaussian gradients)
-    if (MODE != 0 && !DENSE) {
+    if (MODE != 0 && !DENSE && !SMALL) {
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < kOPW; ++j) {
@@ -302,6 +322,22 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
       float tot = warp_sum(ptot[j]);
       if (MODE == 2 && lane == 0 && a.colsum) a.colsum[(int64_t)b * a.C + o] = tot;
       if (DENSE) continue;
+      if constexpr (SMALL) {
+#pragma unroll
+        for (int q = 0; q < NDL; ++q) {
+          if (q >= D) break;
+          const float s0 = warp_sum(acc0[j][q]), s1 = warp_sum(acc1[j][q]);
+          if (lane) continue;
+          if (OWNER_Z) {
+            if (a.gz) a.gz[((int64_t)b * a.Kz + o) * D + q] = a.alpha * s0;
+          } else {
+            const float lam = ov1[ol * SD + q];
+            if (a.gmu) a.gmu[((int64_t)b * a.Kp + o) * D + q] = a.alpha * lam * s0;
+            if (a.glv) a.glv[((int64_t)b * a.Kp + o) * D + q] = a.alpha * 0.5f * (lam * s1 - tot);
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < MAXDL; ++q) {
         const int d = lane + 32 * q;
@@ -316,6 +352,23 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
       }
     }
   }
+}
+
+template <bool ZROWS, int MODE, bool DENSE, int MAXDL>
+__global__ void __launch_bounds__(kThreads) pass_kernel(const PassArgs a) {
+  pass_body<ZROWS, MODE, DENSE, MAXDL>(a);
+}
+
+// The same pass over up to kMaxPassBatch independent edges of one tree level (blockIdx.z = edge):
+// many small edges (e.g. the N data points of a shared-root star) fill the GPU in one
+// launch instead of one under-filled launch each.
+constexpr int kMaxPassBatch = 16;
+struct PassBatch { PassArgs e[kMaxPassBatch]; };
+template <bool ZROWS, int MODE, bool DENSE, int MAXDL>
+__global__ void __launch_bounds__(kThreads) pass_batch_kernel(const __grid_constant__ PassBatch pb) {
+  const PassArgs& a = pb.e[blockIdx.z];
+  if ((int)blockIdx.x * kOPC >= ((MODE != 2) ? a.R : a.C)) return;
+  pass_body<ZROWS, MODE, DENSE, MAXDL>(a);
 }
 
 // ------------------------------------------------------------------------------ small kernels
@@ -364,6 +417,26 @@ __global__ void __launch_bounds__(256) hbuild_kernel(const HBuild h) {
     for (int j = 0; j < h.nchild; ++j) o += h.moff[j][b];
     h.hoff[b] = o;
   }
+}
+
+// Shared-root exchange.  x[b][r] (r < K) accumulates the fp32 residuals of the root's
+// child messages in fp64, x[b][K] their fp64 offsets; `first` overwrites instead of accumulating.
+__global__ void __launch_bounds__(256) xmsg_kernel(const HBuild h, double* x, bool first) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  if (k > h.K) return;
+  double v = first ? 0.0 : x[(int64_t)b * (h.K + 1) + k];
+  for (int j = 0; j < h.nchild; ++j) v += k < h.K ? (double)h.msg[j][(int64_t)b * h.K + k] : h.moff[j][b];
+  x[(int64_t)b * (h.K + 1) + k] = v;
+}
+
+// h_root = u_root + x (x = shard sums of xmsg_kernel, summed over shards by the caller).
+__global__ void __launch_bounds__(256) hroot_kernel(const float* u, const double* uoff, const double* x, int K,
+                                                    float* h, double* hoff) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  if (k < K) h[(int64_t)b * K + k] = u[(int64_t)b * K + k] + (float)x[(int64_t)b * (K + 1) + k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) hoff[b] = uoff[b] + x[(int64_t)b * (K + 1) + K];
 }
 
 // DOWN final: logp = off + LSE_a m[a] - ln K; save lse for the reverse pass.

@@ -46,3 +46,40 @@ def max_over_ranks(values, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(values, op=dist.ReduceOp.MAX, group=group)
     return values
+
+
+# ---------------------------------------------------------------- shared-root star
+# a global latent theta (K_theta samples) shared by N data points.  The data points are
+# sharded over ranks; each rank's graph is the root plus its own children.  The root's incoming
+# messages are additive in the log domain, so ONE all-reduce of a [B][K_theta + 1] fp64 vector per
+# step joins the shards (include/tmc.h, tmc_forward_children / tmc_forward_root).
+def shard_children(N: int, rank: int, world: int) -> List[int]:
+    """Global ids (0-based) of the data points rank `rank` holds: contiguous blocks, the first
+    N % world ranks one larger; a rank may hold none when N < world."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    base, extra = divmod(N, world)
+    start = rank * base + min(rank, extra)
+    return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+def exchange_root_messages(root_msg, group=None):
+    """The one data-path collective of the shared-root star: in-place SUM all-reduce of the
+    shard's root messages (fp64 residual sums and offset sums add across shards)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(root_msg, op=dist.ReduceOp.SUM, group=group)
+    return root_msg
+
+
+def shared_root_estimate(graph, inputs, ws, logp, root_msg, grads=None, dlogp=None, group=None, stream=None):
+    """One sharded TMC evaluation of a shared-root star: children forward -> all-reduce of the
+    root messages -> root elimination (logp, identical on every rank) -> reverse pass of this
+    rank's latents under the global root marginal.  graph.direction must be TMC_DIR_UP."""
+    import paper_1806_08593_b200 as tmc
+    tmc.tmc_forward_children(graph, inputs, root_msg, ws, stream)
+    exchange_root_messages(root_msg, group)
+    tmc.tmc_forward_root(graph, inputs, root_msg, logp, ws, stream)
+    if grads is not None:
+        tmc.tmc_backward(graph, inputs, ws, dlogp, grads, stream=stream)
+    return logp

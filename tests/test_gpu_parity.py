@@ -372,3 +372,60 @@ def test_estimate_host_streamed(torch_cuda, name, kw, chunk):
     for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
         got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
     compare(got, ref, tag="host")
+
+
+@pytest.mark.parametrize("N,K,world", [(5, 3, 2), (2, 3, 3), (64, 128, 4), (7, 300, 2)])
+def test_shared_root_exchange(torch_cuda, N, K, world):
+    """NEXT-2 (P:334-346): the toy-1 star sharded over `world` shards (run one after another here;
+    the sum over shards stands in for the all-reduce).  Every shard's logp equals the oracle's on
+    the full star, and each shard's gradients equal the oracle's for the latents it holds."""
+    import paper_1806_08593_b200 as tmc
+    from paper_1806_08593_b200 import parallel
+    torch = torch_cuda
+    full = tw.make_workload("S_hier", N=N, K=K, B=3)
+    ref = oracle.estimate_workload(full)
+    shards = []
+    total = torch.zeros(full.B, K + 1, dtype=torch.float64, device="cuda")
+    for r in range(world):
+        ids = parallel.shard_children(N, r, world)
+        wl = tw.make_workload("S_hier", N=N, K=K, B=3, children=ids)
+        g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=tmc.TMC_DIR_UP)
+        inp = upload(torch, wl)
+        ws = tmc.alloc_workspace(g)
+        msg = torch.empty(wl.B, K + 1, dtype=torch.float64, device="cuda")
+        tmc.tmc_forward_children(g, inp, msg, ws)
+        total += msg
+        shards.append((ids, g, inp, ws))
+    for ids, g, inp, ws in shards:
+        logp = torch.empty(full.B, dtype=torch.float64, device="cuda")
+        tmc.tmc_forward_root(g, inp, total, logp, ws)
+        gr = tmc.alloc_grads(g)
+        tmc.tmc_backward(g, inp, ws, None, gr)
+        torch.cuda.synchronize()
+        lp = logp.cpu().numpy()
+        assert np.abs(lp - ref["logp"]).max() <= LOGP_TOL
+        lat = [0] + [i + 1 for i in ids]          # global latent index of each local latent
+        for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
+            for j, gl in enumerate(lat):
+                if ref[k][gl] is None:
+                    continue
+                e = rel_err(gr[j][k].cpu().numpy(), ref[k][gl])
+                assert e <= GRAD_TOL, (k, gl, e)
+
+
+def test_shared_root_exchange_single_shard_equals_plain_forward(torch_cuda):
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload("T1_paper", N=16, K=128, B=2)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=tmc.TMC_DIR_UP)
+    inp = upload(torch, wl)
+    ws = tmc.alloc_workspace(g)
+    msg = torch.empty(wl.B, 129, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward_children(g, inp, msg, ws)
+    l1 = torch.empty(wl.B, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward_root(g, inp, msg, l1, ws)
+    l0, _ = tmc.estimate(g, inp, grads=False)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(l1.cpu().numpy(), l0.cpu().numpy(), rtol=0, atol=1e-4)
+    with pytest.raises(tmc.TmcError):          # exchange needs an explicit UP direction
+        tmc.tmc_forward_children(tmc.Graph(wl.parent[:2], wl.K[:2], wl.D[:2], wl.B), inp[:2], msg, ws)

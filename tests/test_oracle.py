@@ -16,7 +16,7 @@ import tmc_workload as tw
 from bruteforce import log_factor, log_weights, pair_marginals, tmc_bruteforce, workload_datapoint
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-TINY = ["S_chain", "S_tree", "S_mnist", "S_mlp", "S_mlp_bern", "C0"]
+TINY = ["S_chain", "S_tree", "S_mnist", "S_mlp", "S_mlp_bern", "S_hier", "C0"]
 
 
 def _f(v):
@@ -252,7 +252,7 @@ def test_unbiased_C0_closed_form():
 
 
 # ----------------------------------------------------------------------------- gradients
-@pytest.mark.parametrize("name", ["S_chain", "S_tree", "S_mnist", "S_mlp"])
+@pytest.mark.parametrize("name", ["S_chain", "S_tree", "S_mnist", "S_mlp", "S_hier"])
 def test_pair_marginals_match_bruteforce(name):
     """dL/dlogf_i = pair marginal of (k_i, k_pa) under normalised weights (autodiff of P:332)."""
     wl = tw.make_workload(name)

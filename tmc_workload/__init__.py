@@ -42,7 +42,7 @@ def rng_for(seed: int, tag: str, b: int = 0, extra: int = 0) -> np.random.Genera
 @dataclasses.dataclass
 class Config:
     name: str
-    family: str                      # "lg" | "mlp_chain" | "mnist"
+    family: str                      # "lg" | "mlp_chain" | "mnist" | "hier"
     B: int
     K: int
     parent: List[int]
@@ -64,6 +64,8 @@ class Config:
     # mnist family extra dims
     enc_hidden: int = 200
     dec_hidden: int = 200
+    # hier family (toy 1): global ids of the data points this shard holds (None = all)
+    children: Optional[List[int]] = None
 
     @property
     def n(self) -> int:
@@ -79,6 +81,10 @@ class Config:
 
 def _chain(n: int) -> List[int]:
     return [-1] + list(range(n - 1))
+
+
+def _star(N: int) -> List[int]:
+    return [-1] + [0] * N
 
 
 def _tree_c4() -> List[int]:
@@ -105,12 +111,19 @@ CONFIGS: Dict[str, Config] = {
     "C4": Config("C4", "lg", B=256, K=512, parent=_tree_c4(), D=[32] * 21, w_var=1.0 / 32,
                  noise_var=0.3, observed=list(range(5, 21)), obs_dim=64, c_var=1.0 / 32,
                  obs_var=0.04, q="prior_marginal"),
+    # the shared-parameter star of P:334-346 on toy 1: theta ~ N(0,1),
+    # z_i | theta ~ N(theta, 1), x_i | z_i ~ N(z_i, 1), i = 1..N; proposals Q(theta) = N(0,1),
+    # Q(z_i) = N(0,2).  One "datapoint" b is one whole data set of N points sharing theta
+    # (B independent replicate data sets); latent 0 = theta, latents 1..N = z_i.
+    "T1": Config("T1", "hier", B=8, K=1024, parent=_star(1024), D=[1] * 1025),
+    "T1_paper": Config("T1_paper", "hier", B=8, K=128, parent=_star(128), D=[1] * 129),
     # ---- shrunk variants of every family (brute-force enumerable)
     "S_chain": Config("S_chain", "lg", B=4, K=3, parent=_chain(4), D=[2] * 4, w_var=0.5,
                       noise_var=0.5, observed=[3], obs_dim=4, obs_var=0.1, q="fixed", q_var=2.0),
     "S_tree": Config("S_tree", "lg", B=4, K=3, parent=[-1, 0, 0, 1, 1], D=[2, 3, 2, 2, 1],
                      w_var=0.5, noise_var=0.3, observed=[2, 3, 4], obs_dim=3, c_var=0.5,
                      obs_var=0.2, q="prior_marginal"),
+    "S_hier": Config("S_hier", "hier", B=3, K=3, parent=_star(3), D=[1] * 4),
     "S_mnist": Config("S_mnist", "mnist", B=4, K=4, parent=[-1, 0], D=[3, 4], hidden=5,
                       enc_hidden=6, dec_hidden=6, obs_dim=16, pixel_p=0.13),
     "S_mlp": Config("S_mlp", "mlp_chain", B=4, K=3, parent=_chain(4), D=[3] * 4, hidden=4,
@@ -121,7 +134,15 @@ CONFIGS: Dict[str, Config] = {
 
 
 def get_config(name: str, **overrides) -> Config:
-    cfg = dataclasses.replace(CONFIGS[name], **overrides)
+    base = CONFIGS[name]
+    if base.family == "hier" and ("N" in overrides or "children" in overrides):
+        # N: data points in the set; children: the global ids a shard holds (star over them)
+        N = overrides.pop("N", base.n - 1)
+        ch = overrides.get("children")
+        m = N if ch is None else len(ch)
+        overrides.update(parent=_star(m), D=[1] * (m + 1))
+        overrides.setdefault("obs_dim", N)
+    cfg = dataclasses.replace(base, **overrides)
     if "K" in overrides or "parent" in overrides or "D" in overrides:
         cfg.name = f"{name}*"
     return cfg
@@ -223,6 +244,8 @@ def make_params(cfg: Config, seed: int = 0) -> dict:
         p["dec"] = _mlp_init(rng, [d1, cfg.dec_hidden, cfg.dec_hidden, cfg.obs_dim])  # p(x|z1)
         p["q_z1"] = _mlp_init(rng, [cfg.obs_dim, cfg.enc_hidden, cfg.enc_hidden, 2 * d1])  # q(z1|x)
         p["q_z2"] = _mlp_init(rng, [d1, H, H, 2 * d2])                       # q(z2|z1)
+    elif cfg.family == "hier":
+        pass                         # no learned parameters in toy 1
     else:
         raise ValueError(cfg.family)
     return p
@@ -241,7 +264,32 @@ def _datapoint(cfg: Config, p: dict, seed: int, b: int):
     lo: list = [None] * n
     xs: list = []
 
-    if cfg.family == "lg":
+    if cfg.family == "hier":
+        # toy 1.  Every draw is keyed by (b, global data-point id) so a shard holding
+        # data points `children` sees exactly the values of the full set.
+        ids = list(range(cfg.n - 1)) if cfg.children is None else list(cfg.children)
+        theta = rd.normal()
+        xs = []
+        for j, gi in enumerate(ids):
+            r = rng_for(seed, "data", b, gi + 1)
+            zi = theta + r.normal()
+            xs.append(zi + r.normal())
+        th = rq.normal(size=(K, 1))                                  # Q(theta) = N(0, 1)
+        z[0] = th.astype(f32)
+        lq[0] = _gauss_logpdf(z[0], 0.0, 1.0).astype(f32)
+        mu[0] = np.zeros((1, 1), f32)                                # prior N(0, 1)
+        lv[0] = np.zeros((1, 1), f32)
+        for j, gi in enumerate(ids):
+            i = j + 1
+            r = rng_for(seed, "prop", b, gi + 1)
+            z[i] = (math.sqrt(2.0) * r.normal(size=(K, 1))).astype(f32)   # Q(z_i) = N(0, 2)
+            lq[i] = _gauss_logpdf(z[i], 0.0, 2.0).astype(f32)
+            mu[i] = z[0].copy()                                      # p(z_i | theta^c) = N(theta^c, 1)
+            lv[i] = np.zeros((K, 1), f32)
+            lo[i] = _gauss_logpdf(np.full((K, 1), xs[j]), z[i].astype(np.float64), 1.0).astype(f32)
+        xs = [np.asarray(xs)]
+
+    elif cfg.family == "lg":
         # data: ancestral draw from the model
         zt = [None] * n
         for i in range(n):
