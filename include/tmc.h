@@ -38,6 +38,7 @@
  *     across streams given distinct workspaces.  Shape/graph/argument errors
  *     are detected synchronously and nothing is launched.  Launch failures
  *     return TMC_ERR_CUDA.  No C++ exception crosses this boundary.
+ *   - B = 0 is valid: nothing is read or launched, and buffer pointers may be NULL.
  *   - -inf is allowed in logq/logobs/logf (probability-zero event).  A
  *     datapoint whose every tuple is impossible gets logp = -inf and all-zero
  *     gradients (never NaN).  NaN inputs are not checked unless TMC_FLAG_VALIDATE.

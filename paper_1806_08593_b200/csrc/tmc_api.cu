@@ -292,6 +292,7 @@ PassArgs edge_args(const Plan& p, int i, const tmc_latent_in* in, const float* c
 
 tmc_status check_inputs(const Plan& p, const tmc_latent_in* in, const float* const* dense) {
   if (!in && !dense) return fail(TMC_ERR_INVALID_ARG, "inputs are NULL");
+  if (p.B == 0) return TMC_OK;            // an empty batch reads no input (empty tensors may be NULL)
   for (int i = 0; i < p.n; ++i) {
     if (dense) {
       if (!dense[i]) return fail(TMC_ERR_INVALID_ARG, "logf_dense[" + std::to_string(i) + "] is NULL");

@@ -460,16 +460,23 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__
     a.cb2[(size_t)b * a.Cpad + c] = v;
     if (v > -INFINITY) s_live[c / kTileRows] = 1;
     if (a.bx) {
-      // row c of the extra operand: k = 0 -> fp16 hi, k = 1 -> fp16 lo of the bias (the constant A
-      // operand has ones there), so the tensor core adds the column bias to S exactly to ~2^-22.
-      // Biases below -60000 (log2 units) contribute exactly 0 anyway; clamp so hi/lo stay finite.
-      const float vc = fmaxf(v, -60000.f);
-      __half hh, ll;
-      split16(vc, hh, ll);
+      // row c of the extra operand: the bias as four fp16-representable parts (each >= -60000 log2
+      // units), every part as fp16 hi + lo in slots k = 2j, 2j+1 (the constant A operand has ones in
+      // k = 0..7), so the tensor core adds the column bias to S to ~2^-22 relative over a range of
+      // 240000 log2 units below the column maximum (a dead column beyond that is clamped there).
+      uint32_t w[4];
+      float rest = fminf(fmaxf(v, -240000.f), 240000.f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float part = (j < 3) ? fminf(fmaxf(rest, -60000.f), 60000.f) : rest;
+        rest -= part;
+        __half hh, ll;
+        split16(part, hh, ll);
+        w[j] = (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
+      }
       uint8_t* tile = a.bx + ((size_t)b * (a.Cpad / kTileRows) + c / kTileRows) * kBxBytes;
       const int r = c % kTileRows;
-      const uint32_t w0 = (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
-      *reinterpret_cast<uint4*>(tile + bx_off(r, 0)) = make_uint4(w0, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(tile + bx_off(r, 0)) = make_uint4(w[0], w[1], w[2], w[3]);
       *reinterpret_cast<uint4*>(tile + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
     }
   }
@@ -560,9 +567,9 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
     for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], G::SOFTMAX_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // constant A operand of the bias MMA: k = 0, 1 are ones (times the bias hi and lo parts)
+  // constant A operand of the bias MMA: k = 0..7 are ones (times the bias parts' hi and lo)
   for (int r = tid; r < kTileRows; r += blockDim.x) {
-    *reinterpret_cast<uint4*>(sAx + bx_off(r, 0)) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sAx + bx_off(r, 0)) = make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
     *reinterpret_cast<uint4*>(sAx + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
   }
   fence_proxy_async();

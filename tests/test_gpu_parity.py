@@ -429,3 +429,89 @@ def test_shared_root_exchange_single_shard_equals_plain_forward(torch_cuda):
     np.testing.assert_allclose(l1.cpu().numpy(), l0.cpu().numpy(), rtol=0, atol=1e-4)
     with pytest.raises(tmc.TmcError):          # exchange needs an explicit UP direction
         tmc.tmc_forward_children(tmc.Graph(wl.parent[:2], wl.K[:2], wl.D[:2], wl.B), inp[:2], msg, ws)
+
+
+# ------------------------------------------------------------------- more edge cases of the boundary
+def _slice_K(wl, Ks):
+    """Per-latent sample counts: keep the first K_i samples of latent i (and the first K_p parent
+    samples of each conditional), a valid workload of the same model with unequal K_i."""
+    z = [wl.z[i][:, :Ks[i]] for i in range(len(Ks))]
+    kp = [1 if wl.parent[i] < 0 else Ks[wl.parent[i]] for i in range(len(Ks))]
+    mu = [wl.mu[i][:, :kp[i]] for i in range(len(Ks))]
+    lv = [wl.logvar[i][:, :kp[i]] for i in range(len(Ks))]
+    lq = [wl.logq[i][:, :Ks[i]] for i in range(len(Ks))]
+    lo = [None if wl.logobs[i] is None else wl.logobs[i][:, :Ks[i]] for i in range(len(Ks))]
+    c = lambda L: [None if a is None else np.ascontiguousarray(a) for a in L]
+    return c(z), c(mu), c(lv), c(lq), c(lo)
+
+
+@pytest.mark.parametrize("name,Ks,direction", [("C3", [300, 130, 257, 129], 0), ("C4", [200, 130, 257, 300, 96], 2),
+                                               ("C3", [1, 300, 7, 256], 0)])
+def test_unequal_K_per_latent(torch_cuda, name, Ks, direction):
+    """K_i may differ per latent: tensor-core and SIMT edges with unequal, ragged K."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    n = len(Ks)
+    base = tw.make_workload(name, B=2, K=max(Ks))
+    parent = base.parent[:n]
+    z, mu, lv, lq, lo = _slice_K(base, Ks)
+    if all(o is None for o in lo):        # keep an observation on the last latent
+        lo[-1] = np.ascontiguousarray(base.logobs[-1][:, :Ks[-1]]) if base.logobs[-1] is not None else None
+    D = base.D[:n]
+    g = tmc.Graph(parent, Ks, D, base.B, direction=direction)
+    t = lambda a: None if a is None else torch.from_numpy(a).cuda()
+    inp = [dict(z=t(z[i]), mu=t(mu[i]), logvar=t(lv[i]), logq=t(lq[i]), logobs=t(lo[i])) for i in range(n)]
+    logp, gr = tmc.estimate(g, inp)
+    torch.cuda.synchronize()
+    ref = oracle.estimate(parent, Ks, D, z, mu, lv, lq, lo)
+    got = {"logp": logp.cpu().numpy()}
+    for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
+        got[k] = [gr[i][k].cpu().numpy() for i in range(n)]
+    compare(got, ref, tag=f"{name}{Ks}")
+
+
+def test_mixed_D_tree_tensor_cores(torch_cuda):
+    """A tree whose sibling edges have D = 32 and D = 64 (batched tensor-core launches grouped by D)
+    plus a D = 48 latent (no tensor-core geometry: SIMT) in the same level."""
+    wl = tw.make_workload("S_tree", B=2, K=200, D=[32, 64, 32, 48, 64], w_var=1 / 64, c_var=1 / 64)
+    got = run_gpu(torch_cuda, wl, precision=0)
+    ref = oracle.estimate_workload(wl)
+    compare(got, ref, tag="mixedD")
+
+
+@pytest.mark.parametrize("precision", [1, 2])
+def test_extreme_dynamic_range(torch_cuda, precision):
+    """Unscaled linear maps at D = 64 (W entries of variance 0.5): |z| up to ~150, logp ~ -3e5 and
+    column biases spanning > 60000 log2 units (beyond one fp16 part of the tensor-core bias
+    operand).  Both paths must stay at fp32 accuracy relative to |logp| (an absolute 1e-3 is below
+    the fp32 ulp of logp here; DESIGN.md §2 R3)."""
+    wl = tw.make_workload("S_tree", B=2, K=200, D=[64] * 5, w_var=0.5, c_var=0.5)
+    got = run_gpu(torch_cuda, wl, precision=precision, grads=False)
+    ref = oracle.estimate_workload(wl, grads=False)
+    rel = np.abs(got["logp"] - ref["logp"]) / np.abs(ref["logp"])
+    assert rel.max() <= 1e-6, rel
+
+
+def test_large_K_single_datapoint(torch_cuda):
+    """K = 8192 (64 tiles per side, 4096 tiles per edge) on the tensor-core path."""
+    wl = tw.make_workload("C3", B=1, K=8192, parent=[-1, 0, 1], D=[32] * 3)
+    got = run_gpu(torch_cuda, wl)
+    ref = oracle.estimate_workload(wl)
+    compare(got, ref, tag="K8192")
+
+
+def test_empty_batch_launches_nothing(torch_cuda):
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload("C3", B=1, K=256)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, 0)
+    e = lambda *s: torch.empty(*s, device="cuda")
+    inp = [dict(z=e(0, 256, 32), mu=e(0, wl.Kp(i), 32), logvar=e(0, wl.Kp(i), 32), logq=e(0, 256),
+                logobs=None if wl.logobs[i] is None else e(0, 256)) for i in range(len(wl.parent))]
+    ws = torch.empty(max(1, tmc.tmc_workspace_size(g)), dtype=torch.uint8, device="cuda")
+    n0 = tmc.tmc_launch_count()
+    logp = torch.empty(0, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward(g, inp, logp, ws)
+    tmc.tmc_backward(g, inp, ws, None, tmc.alloc_grads(g))
+    torch.cuda.synchronize()
+    assert tmc.tmc_launch_count() == n0
