@@ -189,6 +189,17 @@ tmc_status tmc_estimate_host(const tmc_graph *g, const tmc_latent_in *in, double
                              const double *dlogp_host, tmc_latent_grad *out, int32_t chunk, void *ws,
                              size_t ws_bytes, tmc_stream_t stream);
 
+/* Reparameterisation noise for the proposal samples z = mu_q + sigma_q * eps (SURVEY
+ * §8a row a1): eps[b][k][d] ~ N(0, 1), DEVICE fp32 [B][K][D] (16-byte aligned when D % 4 == 0),
+ * for global datapoints b0 .. b0+B-1 of latent `latent`.  Counter-based and bit-exact across
+ * devices, batch splits and world sizes: Philox4x32-10 with key = seed (lo, hi words) and counter
+ * (tag, b0 + b, latent, k * ceil(D/4) + d/4) gives the 4 words of dims 4j..4j+3; each word pair
+ * (w0, w1) -> u = ((w >> 8) + 0.5) 2^-24 -> Box-Muller sqrt(-2 ln u0) (cos, sin)(2 pi u1), with ln,
+ * cos and sin as fixed fp32 polynomials in correctly rounded fma/mul/add/div/sqrt (no libm), so a
+ * host implementation performing the same operations reproduces every bit. */
+tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0, int32_t latent, int32_t K,
+                             int32_t D, float *eps, tmc_stream_t stream);
+
 /* Thread-local message describing the last non-OK status on this thread. */
 const char *tmc_last_error(void);
 

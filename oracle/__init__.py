@@ -13,6 +13,8 @@ Parity status of each routine:
                           W=0 decoupling, MC unbiasedness vs closed-form p(x))
   estimate (gradients) : pinned (brute-force pair marginals, central finite differences
                           of the brute-force value)
+  sample_normal (row a1): pinned (Philox4x32-10 known-answer vectors, ln/cos/sin polynomial
+                          accuracy vs numpy, N(0,1) moments and Kolmogorov-Smirnov)
 """
 from __future__ import annotations
 
@@ -53,6 +55,12 @@ def _load():
         _lib.or_factor.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P]
         _lib.or_estimate.argtypes = ([ctypes.c_int, ctypes.c_int, P, P, P] + [P] * 6 +
                                      [ctypes.c_int, P, P] + [P] * 6 + [ctypes.c_int, ctypes.c_double])
+        _lib.or_sample_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
+        _lib.or_philox4x32_10.argtypes = [P, P, P]
+        _lib.or_log_fp32.restype = ctypes.c_float
+        _lib.or_log_fp32.argtypes = [ctypes.c_float]
+        _lib.or_cos_sin_2pi.argtypes = [ctypes.c_float, P, P]
     return _lib
 
 
@@ -152,6 +160,32 @@ def estimate(parent, K, D, z, mu, logvar, logq, logobs, *, logf_dense=None, dire
     if rc != 0:
         raise ValueError(f"or_estimate failed: {rc}")
     return out
+
+
+def sample_normal(seed: int, tag: int, B: int, b0: int, latent: int, K: int, D: int) -> np.ndarray:
+    """Host definition of the reparameterisation noise (include/tmc.h tmc_sample_normal; row a1)."""
+    out = np.empty((B, K, D), np.float32)
+    if _load().or_sample_normal(int(seed), int(tag), int(B), int(b0), int(latent), int(K), int(D), _ptr(out)) != 0:
+        raise ValueError("or_sample_normal failed")
+    return out
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    o = np.empty(4, np.uint32)
+    _load().or_philox4x32_10(_ptr(c), _ptr(k), _ptr(o))
+    return o
+
+
+def log_fp32(u: float) -> float:
+    return float(_load().or_log_fp32(float(u)))
+
+
+def cos_sin_2pi(v: float):
+    c, s = ctypes.c_float(), ctypes.c_float()
+    _load().or_cos_sin_2pi(float(v), ctypes.byref(c), ctypes.byref(s))
+    return c.value, s.value
 
 
 def estimate_workload(wl, **kw) -> Dict[str, object]:

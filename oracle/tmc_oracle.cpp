@@ -228,6 +228,87 @@ bool is_chain(int n, const int* parent) {
 
 }  // namespace
 
+
+// ============================================================================================
+// the reparameterisation noise eps ~ N(0,1), defined exactly as
+// include/tmc.h (tmc_sample_normal) states it, written here from that definition so the device
+// sampler can be checked bit for bit.  Philox4x32-10 (Salmon et al., SC'11: multipliers
+// 0xD2511F53 / 0xCD9E8D57, Weyl key increments 0x9E3779B9 / 0xBB67AE85, 10 rounds), uniforms
+// ((w >> 8) + 1/2) 2^-24, Box-Muller with ln / cos / sin as the stated fp32 polynomials; every fp32
+// operation below is a single correctly rounded IEEE operation (this file is built with
+// -ffp-contract=off; fma is std::fma).
+namespace a1 {
+
+void philox_4x32_10(const uint32_t in[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+  uint32_t x0 = in[0], x1 = in[1], x2 = in[2], x3 = in[3];
+  for (int round = 0; round < 10; ++round) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * x0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * x2;
+    const uint32_t y0 = (uint32_t)(p1 >> 32) ^ x1 ^ k0;
+    const uint32_t y1 = (uint32_t)p1;
+    const uint32_t y2 = (uint32_t)(p0 >> 32) ^ x3 ^ k1;
+    const uint32_t y3 = (uint32_t)p0;
+    x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+float uniform(uint32_t w) { return ((float)(w >> 8) + 0.5f) * 0x1p-24f; }
+
+float log_fp32(float u) {
+  uint32_t b;
+  std::memcpy(&b, &u, 4);
+  int ex = (int)((b >> 23) & 0xFFu) - 127;
+  const uint32_t mb = (b & 0x7FFFFFu) | 0x3F800000u;
+  float m;
+  std::memcpy(&m, &mb, 4);
+  if (m > 0x1.6a09e6p+0f) {          // fp32(sqrt 2)
+    m = m * 0.5f;
+    ex = ex + 1;
+  }
+  const float t = (m - 1.0f) / (m + 1.0f);
+  const float t2 = t * t;
+  // 1 + t^2/3 + t^4/5 + ... + t^12/13, Horner from the top, coefficients fp32(1/(2j+1))
+  const float coef[6] = {0x1.3b13b2p-4f, 0x1.745d18p-4f, 0x1.c71c72p-4f, 0x1.24924ap-3f, 0x1.99999ap-3f, 0x1.555556p-2f};
+  float h = coef[0];
+  for (int j = 1; j < 6; ++j) h = std::fma(h, t2, coef[j]);
+  h = std::fma(h, t2, 1.0f);
+  const float lm = (2.0f * t) * h;
+  return std::fma((float)ex, 0x1.62e430p-1f, lm);     // fp32(ln 2)
+}
+
+void cos_sin_2pi(float v, float* c, float* s) {
+  const float q = std::nearbyint(v * 4.0f);
+  const float w = v + q * -0.25f;
+  const float x = w * 0x1.921fb6p+2f;                  // fp32(2 pi)
+  const float x2 = x * x;
+  const float sc[5] = {-0x1.ae6456p-26f, 0x1.71de3ap-19f, -0x1.a01a02p-13f, 0x1.111112p-7f, -0x1.555556p-3f};
+  float sp = sc[0];
+  for (int j = 1; j < 5; ++j) sp = std::fma(sp, x2, sc[j]);
+  sp = std::fma(sp * x2, x, x);                         // x - x^3/3! + ... - x^11/11!
+  const float cc[7] = {0x1.1eed8ep-29f, -0x1.27e4fcp-22f, 0x1.a01a02p-16f, -0x1.6c16c2p-10f, 0x1.555556p-5f, -0.5f, 1.0f};
+  float cp = cc[0];
+  for (int j = 1; j < 7; ++j) cp = std::fma(cp, x2, cc[j]);   // 1 - x^2/2! + ... + x^12/12!
+  switch (((int)q) & 3) {
+    case 0: *c = cp; *s = sp; break;
+    case 1: *c = -sp; *s = cp; break;
+    case 2: *c = -cp; *s = -sp; break;
+    default: *c = sp; *s = -cp; break;
+  }
+}
+
+void gauss_pair(uint32_t w0, uint32_t w1, float* n0, float* n1) {
+  const float r = std::sqrt(-2.0f * log_fp32(uniform(w0)));
+  float c, s;
+  cos_sin_2pi(uniform(w1), &c, &s);
+  *n0 = r * c;
+  *n1 = r * s;
+}
+
+}  // namespace a1
+
 extern "C" {
 
 // Joint-max logsumexp of x[0..n).  Returns -inf for n == 0.
@@ -289,5 +370,29 @@ int or_estimate(int n, int B, const int* parent, const int* K, const int* D,
   for (auto& x : th) x.join();
   return 0;
 }
+
+
+// eps[b][k][d], b = 0..B-1 <-> global datapoint b0 + b (tmc_sample_normal's definition).
+int or_sample_normal(uint64_t seed, uint32_t tag, int B, int64_t b0, int latent, int K, int D, float* eps) {
+  if (B < 0 || K < 0 || D <= 0 || !eps) return -1;
+  const int groups = (D + 3) / 4;
+  for (int b = 0; b < B; ++b)
+    for (int k = 0; k < K; ++k)
+      for (int g = 0; g < groups; ++g) {
+        const uint32_t ctr[4] = {tag, (uint32_t)(b0 + b), (uint32_t)latent, (uint32_t)(k * groups + g)};
+        uint32_t w[4];
+        a1::philox_4x32_10(ctr, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), w);
+        float e[4];
+        a1::gauss_pair(w[0], w[1], &e[0], &e[1]);
+        a1::gauss_pair(w[2], w[3], &e[2], &e[3]);
+        for (int q = 0; q < 4 && 4 * g + q < D; ++q) eps[((size_t)b * K + k) * D + 4 * g + q] = e[q];
+      }
+  return 0;
+}
+
+// Raw Philox4x32-10 (known-answer tests) and the fp32 polynomials (accuracy pins).
+void or_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) { a1::philox_4x32_10(ctr, key[0], key[1], out); }
+float or_log_fp32(float u) { return a1::log_fp32(u); }
+void or_cos_sin_2pi(float v, float* c, float* s) { a1::cos_sin_2pi(v, c, s); }
 
 }  // extern "C"

@@ -24,7 +24,7 @@ STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_
           -7: "TMC_ERR_CUDA", -8: "TMC_ERR_NONFINITE"}
 
 EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate",
-           "tmc_forward_children", "tmc_forward_root",
+           "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal",
            "tmc_estimate_host_workspace_size", "tmc_estimate_host",
            "tmc_last_error", "tmc_version", "tmc_launch_count"]
 
@@ -76,8 +76,10 @@ def load_library(path: str = LIB_PATH):
                                           ctypes.c_int32, P, ctypes.c_size_t, P]
         lib.tmc_forward_children.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, ctypes.c_size_t, P]
         lib.tmc_forward_root.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, P, ctypes.c_size_t, P]
+        lib.tmc_sample_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int64,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P]
         for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate", "tmc_estimate_host",
-                  "tmc_forward_children", "tmc_forward_root"):
+                  "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal"):
             getattr(lib, f).restype = ctypes.c_int
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
@@ -202,6 +204,17 @@ def tmc_forward_root(graph: Graph, inputs: List[Dict], root_msg_total, logp, ws,
     """Shared-root exchange step 3: the root's elimination from the shard-summed root_msg."""
     _check(load_library().tmc_forward_root(graph.ref(), _inputs(inputs), _dp(root_msg_total), _dp(logp),
                                            _dp(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+# stream tags of the counter-based draws (SURVEY §8c A12)
+TAG_PARAMS, TAG_DATA, TAG_PROPOSAL_PARAMS, TAG_EPS, TAG_MC = 1, 2, 3, 4, 5
+
+
+def tmc_sample_normal(seed: int, tag: int, b0: int, latent: int, eps, stream=None) -> None:
+    """eps (device fp32 [B][K][D], contiguous) <- N(0,1) draws of global datapoints b0.. (row a1)."""
+    B, K, D = eps.shape
+    _check(load_library().tmc_sample_normal(int(seed), int(tag), int(B), int(b0), int(latent), int(K), int(D),
+                                            _dp(eps), _stream(stream)))
 
 
 def tmc_estimate_host_workspace_size(graph: Graph, chunk: int) -> int:

@@ -13,6 +13,7 @@
 
 #include "../../include/tmc.h"
 #include "tmc_internal.h"
+#include "tmc_sample.cuh"
 #include "tmc_simt.cuh"
 #include "tmc_tc.cuh"
 
@@ -765,6 +766,33 @@ tmc_status tmc_forward_root(const tmc_graph* g, const tmc_latent_in* in, const d
     if (st != TMC_OK) return st;
     if ((!root_msg_total || !logp) && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "root_msg_total / logp is NULL");
     return forward_impl(p, in, nullptr, logp, ws, reinterpret_cast<cudaStream_t>(stream), 2, nullptr, root_msg_total);
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0, int32_t latent, int32_t K, int32_t D,
+                             float* eps, tmc_stream_t stream) {
+  try {
+    if (B < 0 || K < 0 || D <= 0 || b0 < 0 || latent < 0) return fail(TMC_ERR_SHAPE, "tmc_sample_normal: bad shape");
+    if ((int64_t)B * K == 0) return TMC_OK;
+    if (!eps) return fail(TMC_ERR_INVALID_ARG, "eps is NULL");
+    if (reinterpret_cast<uintptr_t>(eps) % 4) return fail(TMC_ERR_ALIGNMENT, "eps must be 4-byte aligned");
+    tmc_status st = check_device();
+    if (st != TMC_OK) return st;
+    if ((D & 3) == 0 && reinterpret_cast<uintptr_t>(eps) % 16)
+      return fail(TMC_ERR_ALIGNMENT, "eps must be 16-byte aligned when D % 4 == 0");
+    const int64_t n = (int64_t)B * K * ((D + 3) / 4);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16);
+    rng::normal_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(seed, tag, B, b0, latent, K, D, eps);
+    TMC_COUNT_LAUNCH();
+    return launch_check("tmc_sample_normal");
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }

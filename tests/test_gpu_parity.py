@@ -515,3 +515,43 @@ def test_empty_batch_launches_nothing(torch_cuda):
     tmc.tmc_backward(g, inp, ws, None, tmc.alloc_grads(g))
     torch.cuda.synchronize()
     assert tmc.tmc_launch_count() == n0
+
+
+@pytest.mark.parametrize("B,b0,latent,K,D", [(3, 0, 0, 2048, 32), (2, 5, 7, 37, 5), (1, 1023, 2, 20, 100),
+                                            (4, 0, 1, 1, 1), (2, 3, 4, 257, 64)])
+def test_sample_normal_bit_exact(torch_cuda, B, b0, latent, K, D):
+    """Row a1 (A22): the device sampler reproduces the host definition bit for bit."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    eps = torch.empty(B, K, D, device="cuda")
+    tmc.tmc_sample_normal(0x1234_5678_9ABC, tmc.TAG_EPS, b0, latent, eps)
+    torch.cuda.synchronize()
+    ref = oracle.sample_normal(0x1234_5678_9ABC, tmc.TAG_EPS, B, b0, latent, K, D)
+    assert np.array_equal(eps.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_harness_fresh_noise_is_the_sampler(torch_cuda):
+    """The training-step harness draws its reparameterisation noise with tmc_sample_normal on the
+    device: a shard's eps equals the host definition for its global datapoint ids, and the TMC
+    estimate on the resulting model inputs matches the oracle."""
+    import paper_1806_08593_b200 as tmc
+    from tmc_workload.torch_model import TorchModel
+    torch = torch_cuda
+    cfg = tw.get_config("S_mlp", B=6, K=5)
+    wl = tw.make_workload(cfg, b_ids=[2, 3, 4])
+    m = TorchModel(wl, "cuda")
+    m.fresh_noise(99)
+    for i, e in enumerate(m.eps):
+        ref = oracle.sample_normal(99, tmc.TAG_EPS, 3, 2, i, cfg.K, cfg.D[i])
+        assert np.array_equal(e.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    f = m.forward()
+    inp = [dict(z=f["z"][i].detach(), mu=f["mu"][i].detach(), logvar=f["logvar"][i].detach(),
+                logq=f["logq"][i].detach(), logobs=None if f["logobs"][i] is None else f["logobs"][i].detach())
+           for i in range(cfg.n)]
+    g = tmc.Graph(cfg.parent, [cfg.K] * cfg.n, cfg.D, 3)
+    logp, _ = tmc.estimate(g, inp, grads=False)
+    c = lambda t: None if t is None else t.cpu().numpy()
+    ref = oracle.estimate(cfg.parent, [cfg.K] * cfg.n, cfg.D, [c(x["z"]) for x in inp], [c(x["mu"]) for x in inp],
+                          [c(x["logvar"]) for x in inp], [c(x["logq"]) for x in inp], [c(x["logobs"]) for x in inp],
+                          grads=False)
+    assert np.abs(logp.cpu().numpy() - ref["logp"]).max() <= LOGP_TOL

@@ -381,3 +381,49 @@ def test_dregs_surrogate_identity():
                 g[idx] = np.sum(c * (lwz(zp) - lwz(zm)) / (2 * h))
             scale = 0.5 * math.exp(r2["logp"][b] - 2 * r1["logp"][b] - lnK)
             np.testing.assert_allclose(scale * r2["dz"][j][b], g, rtol=1e-5, atol=1e-7)
+
+
+# ----------------------------------------------------------------------------- row a1: sampling
+def test_philox_known_answers():
+    """Philox4x32-10 against the published known-answer vectors (tests/golden/philox_kat.json)."""
+    kat = json.load(open(os.path.join(GOLDEN, "philox_kat.json")))["vectors"]
+    for v in kat:
+        h = lambda xs: [int(x, 16) for x in xs]
+        assert oracle.philox4x32_10(h(v["ctr"]), h(v["key"])).tolist() == h(v["out"])
+
+
+def test_box_muller_polynomials_accuracy():
+    """The fixed fp32 ln / cos / sin polynomials of the sampler definition against numpy (fp64)."""
+    u = np.concatenate([np.linspace(2.0 ** -24, 1.0, 20001), 2.0 ** -np.arange(1, 25)]).astype(np.float32)
+    got = np.array([oracle.log_fp32(x) for x in u], np.float64)
+    ref = np.log(u.astype(np.float64))
+    assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)) <= 1e-6 or np.max(np.abs(got - ref)) <= 2e-7
+    assert np.max(np.abs(got - ref)) <= 4e-6                 # |ln u| <= 16.6: a few fp32 ulps
+    v = np.linspace(0.0, 1.0, 20001, endpoint=False).astype(np.float32)
+    cs = np.array([oracle.cos_sin_2pi(x) for x in v], np.float64)
+    ang = 2 * np.pi * v.astype(np.float64)
+    assert np.max(np.abs(cs[:, 0] - np.cos(ang))) <= 1e-6
+    assert np.max(np.abs(cs[:, 1] - np.sin(ang))) <= 1e-6
+
+
+def test_sample_normal_distribution_and_keying():
+    """eps ~ N(0,1): moments and Kolmogorov-Smirnov on 2^20 draws; the draws of a datapoint do not
+    depend on which batch slice produced them (counter = global id); ragged D uses a prefix of the
+    4-wide group."""
+    from scipy.stats import kstest
+    e = oracle.sample_normal(7, 4, 64, 0, 3, 1024, 16).ravel().astype(np.float64)
+    n = e.size
+    assert abs(e.mean()) <= 5 / math.sqrt(n)
+    assert abs(e.var() - 1) <= 5 * math.sqrt(2 / n)
+    assert kstest(e, "norm").pvalue > 1e-3
+    full = oracle.sample_normal(7, 4, 10, 0, 1, 33, 5)
+    part = oracle.sample_normal(7, 4, 3, 6, 1, 33, 5)
+    assert np.array_equal(full[6:9], part)
+    d8 = oracle.sample_normal(7, 4, 2, 0, 1, 3, 8)
+    d5 = oracle.sample_normal(7, 4, 2, 0, 1, 3, 5)
+    assert np.array_equal(d8[..., :5], d5)       # same ceil(D/4): D = 5 is a prefix of D = 8
+    d9 = oracle.sample_normal(7, 4, 2, 0, 1, 3, 9)
+    assert np.array_equal(d9[:, 0, :8], d8[:, 0])   # k = 0 shares counters; k >= 1 moves with ceil(D/4)
+    assert not np.array_equal(d9[:, 1, :8], d8[:, 1])
+    other = oracle.sample_normal(8, 4, 10, 0, 1, 33, 5)
+    assert not np.any(other == full)

@@ -57,6 +57,22 @@ class TorchModel:
             self.logq_fixed = [t(wl.logq[i]) for i in range(n)]
             self.x = {i: t(np.stack([xs[k] for xs in wl.x])) for k, i in enumerate(sorted(p["C"]))}
         self.grad_numel = sum(x.numel() for x in self.params)
+        self.b0 = int(wl.b_ids[0]) if len(wl.b_ids) else 0
+        if len(wl.b_ids) and not np.array_equal(wl.b_ids, np.arange(self.b0, self.b0 + len(wl.b_ids))):
+            self.b0 = None                    # device noise needs a contiguous block of global ids
+
+    def fresh_noise(self, seed: int) -> None:
+        """Redraw the reparameterisation noise on the device with libtmc's
+        counter-based sampler: eps_i[b,k,:] is keyed by (seed, tag eps, global datapoint b,
+        latent i, k), so every rank draws its own shard's noise and a datapoint's noise does not
+        depend on the world size.  A training step calls this with a new seed each step."""
+        import paper_1806_08593_b200 as tmc
+        if self.cfg.family != "mlp_chain":
+            return                            # lg proposals are fixed samples (no reparameterisation)
+        if self.b0 is None:
+            raise ValueError("fresh_noise needs contiguous global datapoint ids")
+        for i, e in enumerate(self.eps):
+            tmc.tmc_sample_normal(seed, tmc.TAG_EPS, self.b0, i, e)
 
     @staticmethod
     def _mlp(layers, h):
