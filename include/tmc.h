@@ -189,6 +189,19 @@ tmc_status tmc_estimate_host(const tmc_graph *g, const tmc_latent_in *in, double
                              const double *dlogp_host, tmc_latent_grad *out, int32_t chunk, void *ws,
                              size_t ws_bytes, tmc_stream_t stream);
 
+/* IWAE at equal K on the same inputs, for side-by-side cost and
+ * bound comparisons with TMC: the K joint samples are the index tuples (k, ..., k) (latent i's k-th
+ * sample, its conditional at the parent's k-th sample, a root at its prior row 0):
+ *   logp[b] = log (1/K) sum_k exp( sum_i [log N(z_i[b,k]; mu_i[b,c], e^{v_i[b,c]}) - logq_i[b,k] + logobs_i[b,k]] ),
+ * c = k (root: 0), times factor_power like tmc_forward.  Requires K_i equal on every latent
+ * (else TMC_ERR_SHAPE).  out (may be NULL) receives the gradient of J = sum_b dlogp[b] logp[b]
+ * in tmc_latent_grad's layout; only the diagonal rows c = k of dmu/dlogvar are written (the other
+ * rows have zero gradient and are left untouched); pair_marginal is ignored.
+ * ws: DEVICE workspace of tmc_iwae_workspace_size(g) bytes. */
+size_t tmc_iwae_workspace_size(const tmc_graph *g);
+tmc_status tmc_iwae(const tmc_graph *g, const tmc_latent_in *in, double *logp, const double *dlogp,
+                    tmc_latent_grad *out, void *ws, size_t ws_bytes, tmc_stream_t stream);
+
 /* Reparameterisation noise for the proposal samples z = mu_q + sigma_q * eps (SURVEY
  * §8a row a1): eps[b][k][d] ~ N(0, 1), DEVICE fp32 [B][K][D] (16-byte aligned when D % 4 == 0),
  * for global datapoints b0 .. b0+B-1 of latent `latent`.  Counter-based and bit-exact across

@@ -13,6 +13,8 @@ Parity status of each routine:
                           W=0 decoupling, MC unbiasedness vs closed-form p(x))
   estimate (gradients) : pinned (brute-force pair marginals, central finite differences
                           of the brute-force value)
+  iwae (NEXT-3)        : pinned (diagonal tuples of the brute-force enumeration, finite
+                          differences of that value, K=1 == TMC K=1, E[exp L] = p(x) on C0)
   sample_normal (row a1): pinned (Philox4x32-10 known-answer vectors, ln/cos/sin polynomial
                           accuracy vs numpy, N(0,1) moments and Kolmogorov-Smirnov)
 """
@@ -55,6 +57,7 @@ def _load():
         _lib.or_factor.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P]
         _lib.or_estimate.argtypes = ([ctypes.c_int, ctypes.c_int, P, P, P] + [P] * 6 +
                                      [ctypes.c_int, P, P] + [P] * 6 + [ctypes.c_int, ctypes.c_double])
+        _lib.or_iwae.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P] + [P] * 5 + [P, P] + [P] * 5
         _lib.or_sample_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_int64,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
         _lib.or_philox4x32_10.argtypes = [P, P, P]
@@ -159,6 +162,37 @@ def estimate(parent, K, D, z, mu, logvar, logq, logobs, *, logf_dense=None, dire
         arr(pr), arr(gz), arr(gmu), arr(gv), arr(gq), arr(go), int(nt), float(alpha))
     if rc != 0:
         raise ValueError(f"or_estimate failed: {rc}")
+    return out
+
+
+def iwae(parent, K, D, z, mu, logvar, logq, logobs, dlogp=None, grads=True) -> Dict[str, object]:
+    """IWAE at equal K by its definition, fp64, with gradients."""
+    p, k, d = _graph(parent, K, D)
+    n = len(p)
+    f32 = lambda lst: None if lst is None else [None if a is None else np.ascontiguousarray(a, np.float32) for a in lst]
+    z, mu, logvar, logq, logobs = f32(z), f32(mu), f32(logvar), f32(logq), f32(logobs)
+    B = z[0].shape[0]
+    Kp = [1 if p[i] < 0 else int(k[p[i]]) for i in range(n)]
+    out: Dict[str, object] = {"logp": np.empty(B, np.float64)}
+    keep = []
+
+    def arr(lst):
+        b, a = _ptr_array(lst)
+        keep.append(a)
+        return b
+    gz = gmu = gv = gq = go = None
+    if grads:
+        gz = [np.zeros((B, k[i], d[i])) for i in range(n)]
+        gmu = [np.zeros((B, Kp[i], d[i])) for i in range(n)]
+        gv = [np.zeros((B, Kp[i], d[i])) for i in range(n)]
+        gq = [np.zeros((B, k[i])) for i in range(n)]
+        go = [np.zeros((B, k[i])) for i in range(n)]
+        out.update(dz=gz, dmu=gmu, dlogvar=gv, dlogq=gq, dlogobs=go)
+    dl = None if dlogp is None else np.ascontiguousarray(dlogp, np.float64)
+    rc = _load().or_iwae(n, B, _ptr(p), _ptr(k), _ptr(d), arr(z), arr(mu), arr(logvar), arr(logq), arr(logobs),
+                         _ptr(dl), _ptr(out["logp"]), arr(gz), arr(gmu), arr(gv), arr(gq), arr(go))
+    if rc != 0:
+        raise ValueError(f"or_iwae failed: {rc}")
     return out
 
 

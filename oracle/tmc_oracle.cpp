@@ -395,4 +395,67 @@ void or_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
 float or_log_fp32(float u) { return a1::log_fp32(u); }
 void or_cos_sin_2pi(float v, float* c, float* s) { a1::cos_sin_2pi(v, c, s); }
 
+
+// NEXT-3: the IWAE estimator at equal K, by its definition: the K joint
+// samples are the index tuples (k, k, ..., k) (every latent's k-th sample, its conditional taken at
+// the parent's k-th sample), log w_k = sum_i [log p(z_i^k | z_pa^k) - log q_i(z_i^k) + log p(x_i | z_i^k)],
+// L = log (1/K) sum_k w_k.  Gradients of J = sum_b dlogp[b] L_b: with pi_k = dlogp * softmax_k(log w),
+// dlogobs_i[k] = pi_k, dlogq_i[k] = -pi_k, and the Gaussian terms of the (k, k) pair of each edge.
+// All K_i must be equal.  Returns 0, -1 bad graph / unequal K.
+int or_iwae(int n, int B, const int* parent, const int* K, const int* D,
+            const float* const* z, const float* const* mu, const float* const* logvar,
+            const float* const* logq, const float* const* logobs, const double* dlogp, double* logp,
+            double* const* dz, double* const* dmu, double* const* dlogvar, double* const* dlogq,
+            double* const* dlogobs) {
+  if (!valid_graph(n, B, parent, K, D) || !logp) return -1;
+  for (int i = 1; i < n; ++i)
+    if (K[i] != K[0]) return -1;
+  const int Kk = K[0];
+  for (int b = 0; b < B; ++b) {
+    std::vector<double> lw(Kk, 0.0);
+    for (int k = 0; k < Kk; ++k) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const int c = parent[i] < 0 ? 0 : k;
+        const int Kp = parent[i] < 0 ? 1 : K[parent[i]];
+        const size_t zo = ((size_t)b * K[i] + k) * D[i], mo = ((size_t)b * Kp + c) * D[i];
+        s += log_normal_pair(z[i] + zo, mu[i] + mo, logvar[i] + mo, D[i]);
+        s -= (double)logq[i][(size_t)b * K[i] + k];
+        if (logobs && logobs[i]) s += (double)logobs[i][(size_t)b * K[i] + k];
+      }
+      lw[k] = s;
+    }
+    double M = -std::numeric_limits<double>::infinity();
+    for (double v : lw) M = std::max(M, v);
+    double S = 0.0;
+    if (M > -std::numeric_limits<double>::infinity())
+      for (double v : lw) S += std::exp(v - M);
+    logp[b] = (M == -std::numeric_limits<double>::infinity()) ? M : M + std::log(S) - std::log((double)Kk);
+    const double wb = dlogp ? dlogp[b] : 1.0;
+    for (int i = 0; i < n; ++i) {
+      const int Kp = parent[i] < 0 ? 1 : K[parent[i]];
+      if (dmu && dmu[i]) std::fill(dmu[i] + (size_t)b * Kp * D[i], dmu[i] + (size_t)(b + 1) * Kp * D[i], 0.0);
+      if (dlogvar && dlogvar[i]) std::fill(dlogvar[i] + (size_t)b * Kp * D[i], dlogvar[i] + (size_t)(b + 1) * Kp * D[i], 0.0);
+    }
+    for (int k = 0; k < Kk; ++k) {
+      const double pk = (S > 0.0) ? wb * std::exp(lw[k] - M) / S : 0.0;
+      for (int i = 0; i < n; ++i) {
+        const int c = parent[i] < 0 ? 0 : k;
+        const int Kp = parent[i] < 0 ? 1 : K[parent[i]];
+        const size_t zo = ((size_t)b * K[i] + k) * D[i], mo = ((size_t)b * Kp + c) * D[i];
+        if (dlogobs && dlogobs[i]) dlogobs[i][(size_t)b * K[i] + k] = pk;
+        if (dlogq && dlogq[i]) dlogq[i][(size_t)b * K[i] + k] = -pk;
+        for (int d = 0; d < D[i]; ++d) {
+          const double diff = (double)z[i][zo + d] - (double)mu[i][mo + d];
+          const double lam = std::exp(-(double)logvar[i][mo + d]);
+          if (dz && dz[i]) dz[i][zo + d] = -pk * diff * lam;
+          if (dmu && dmu[i]) dmu[i][mo + d] += pk * diff * lam;
+          if (dlogvar && dlogvar[i]) dlogvar[i][mo + d] += 0.5 * pk * (diff * diff * lam - 1.0);
+        }
+      }
+    }
+  }
+  return 0;
+}
+
 }  // extern "C"

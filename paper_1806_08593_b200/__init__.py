@@ -25,6 +25,7 @@ STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_
 
 EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate",
            "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal",
+           "tmc_iwae_workspace_size", "tmc_iwae",
            "tmc_estimate_host_workspace_size", "tmc_estimate_host",
            "tmc_last_error", "tmc_version", "tmc_launch_count"]
 
@@ -78,8 +79,12 @@ def load_library(path: str = LIB_PATH):
         lib.tmc_forward_root.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, P, ctypes.c_size_t, P]
         lib.tmc_sample_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int64,
                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P]
+        lib.tmc_iwae_workspace_size.restype = ctypes.c_size_t
+        lib.tmc_iwae_workspace_size.argtypes = [G]
+        lib.tmc_iwae.argtypes = [G, ctypes.POINTER(tmc_latent_in), P, P, ctypes.POINTER(tmc_latent_grad), P,
+                                 ctypes.c_size_t, P]
         for f in ("tmc_factors", "tmc_forward", "tmc_backward", "tmc_estimate", "tmc_estimate_host",
-                  "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal"):
+                  "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal", "tmc_iwae"):
             getattr(lib, f).restype = ctypes.c_int
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
@@ -204,6 +209,29 @@ def tmc_forward_root(graph: Graph, inputs: List[Dict], root_msg_total, logp, ws,
     """Shared-root exchange step 3: the root's elimination from the shard-summed root_msg."""
     _check(load_library().tmc_forward_root(graph.ref(), _inputs(inputs), _dp(root_msg_total), _dp(logp),
                                            _dp(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def tmc_iwae(graph: Graph, inputs: List[Dict], logp, dlogp, grads: Optional[List[Dict]], ws, stream=None) -> None:
+    """IWAE at equal K on the TMC inputs (NEXT-3): logp [B] fp64 and, if grads, input gradients."""
+    _check(load_library().tmc_iwae(graph.ref(), _inputs(inputs), _dp(logp), _dp(dlogp),
+                                   None if grads is None else _grads(grads, graph.n), _dp(ws),
+                                   ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def iwae(graph: Graph, inputs: List[Dict], dlogp=None, grads: bool = True, stream=None):
+    """Convenience: (logp, grads) of the IWAE estimator; dmu/dlogvar are zero-initialised."""
+    import torch
+    dev = inputs[0]["z"].device
+    logp = torch.empty(graph.B, dtype=torch.float64, device=dev)
+    ws = torch.empty(max(1, load_library().tmc_iwae_workspace_size(graph.ref())), dtype=torch.uint8, device=dev)
+    g = None
+    if grads:
+        g = alloc_grads(graph, dev)
+        for e in g:
+            e["dmu"].zero_()
+            e["dlogvar"].zero_()
+    tmc_iwae(graph, inputs, logp, dlogp, g, ws, stream)
+    return logp, g
 
 
 # stream tags of the counter-based draws (SURVEY §8c A12)

@@ -13,6 +13,7 @@
 
 #include "../../include/tmc.h"
 #include "tmc_internal.h"
+#include "tmc_iwae.cuh"
 #include "tmc_sample.cuh"
 #include "tmc_simt.cuh"
 #include "tmc_tc.cuh"
@@ -793,6 +794,71 @@ tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0,
     rng::normal_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(seed, tag, B, b0, latent, K, D, eps);
     TMC_COUNT_LAUNCH();
     return launch_check("tmc_sample_normal");
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+size_t tmc_iwae_workspace_size(const tmc_graph* g) {
+  if (!g || g->n <= 0 || g->B < 0 || !g->K) return 0;
+  return (size_t)std::max(g->B, 1) * (size_t)std::max(g->K[0], 1) * sizeof(double);
+}
+
+tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, const double* dlogp,
+                    tmc_latent_grad* out, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    Plan p;
+    tmc_status st = make_plan(g, false, p);
+    if (st != TMC_OK) return st;
+    for (int i = 0; i < p.n; ++i) {
+      if (p.K[i] != p.K[0]) return fail(TMC_ERR_SHAPE, "tmc_iwae needs equal K on every latent");
+      if (p.parent[i] < 0 && p.D[i] > 32 * iwae::kRootMaxChunks) return fail(TMC_ERR_SHAPE, "tmc_iwae: root D > 256");
+    }
+    if ((st = check_inputs(p, in, nullptr)) != TMC_OK) return st;
+    if (p.B == 0) return TMC_OK;
+    if (!logp) return fail(TMC_ERR_INVALID_ARG, "logp is NULL");
+    const size_t need = tmc_iwae_workspace_size(g);
+    if (!ws || ws_bytes < need) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    if ((st = check_device()) != TMC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    double* w = static_cast<double*>(ws);
+    const int K = p.K[0];
+    auto fill = [&](int i0, int cnt, iwae::Batch& bt) {
+      bt = iwae::Batch{};
+      bt.count = cnt; bt.B = p.B; bt.K = K; bt.alpha = p.alpha;
+      int roots = 0;
+      for (int j = 0; j < cnt; ++j) {
+        const int i = i0 + j;
+        iwae::LatDesc& L = bt.l[j];
+        L.z = in[i].z; L.mu = in[i].mu; L.lv = in[i].logvar; L.logq = in[i].logq; L.logobs = in[i].logobs;
+        if (out) { L.gz = out[i].dz; L.gmu = out[i].dmu; L.glv = out[i].dlogvar; L.gq = out[i].dlogq; L.go = out[i].dlogobs; }
+        L.D = p.D[i]; L.root = p.parent[i] < 0;
+        roots += L.root;
+      }
+      return roots;
+    };
+    const unsigned grid = (unsigned)(((int64_t)p.B * K + 7) / 8);     // one warp per (b, k) row
+    for (int i0 = 0; i0 < p.n; i0 += iwae::kMaxLat) {
+      iwae::Batch bt;
+      fill(i0, std::min(iwae::kMaxLat, p.n - i0), bt);
+      iwae::logw_kernel<<<grid, 256, 0, s>>>(bt, w, i0 == 0);
+      TMC_COUNT_LAUNCH();
+    }
+    iwae::lse_kernel<<<p.B, 256, 0, s>>>(w, K, dlogp, logp);
+    TMC_COUNT_LAUNCH();
+    if (out) {
+      for (int i0 = 0; i0 < p.n; i0 += iwae::kMaxLat) {
+        iwae::Batch bt;
+        const int roots = fill(i0, std::min(iwae::kMaxLat, p.n - i0), bt);
+        iwae::grad_kernel<<<grid, 256, 0, s>>>(bt, w);
+        TMC_COUNT_LAUNCH();
+        if (roots) {
+          iwae::root_grad_kernel<<<dim3(p.B, roots), 256, 0, s>>>(bt, w);
+          TMC_COUNT_LAUNCH();
+        }
+      }
+    }
+    return launch_check("tmc_iwae");
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }

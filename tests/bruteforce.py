@@ -64,3 +64,12 @@ def workload_datapoint(wl, b):
     fac = [log_factor(wl.z[i][b], wl.mu[i][b], wl.logvar[i][b], wl.logq[i][b]) for i in range(n)]
     obs = [None if wl.logobs[i] is None else np.asarray(wl.logobs[i][b], np.float64) for i in range(n)]
     return fac, obs
+
+
+def iwae_bruteforce(parent, K, factors, obs):
+    """IWAE at equal K by definition: the K joint samples are the tuples (k, ..., k)."""
+    n = len(parent)
+    Kk = K[0]
+    lw = np.array([sum(factors[i][k, 0 if parent[i] < 0 else k] + (0.0 if obs[i] is None else obs[i][k])
+                       for i in range(n)) for k in range(Kk)])
+    return logsumexp(lw) - math.log(Kk)

@@ -555,3 +555,21 @@ def test_harness_fresh_noise_is_the_sampler(torch_cuda):
                           [c(x["logvar"]) for x in inp], [c(x["logq"]) for x in inp], [c(x["logobs"]) for x in inp],
                           grads=False)
     assert np.abs(logp.cpu().numpy() - ref["logp"]).max() <= LOGP_TOL
+
+
+@pytest.mark.parametrize("name,kw", [("C0", {}), ("S_tree", {}), ("C2", dict(B=3, K=70)), ("C3", dict(B=2, K=300)),
+                                     ("C4", dict(B=2, K=130)), ("C1", dict(B=3, K=20)), ("S_hier", dict(N=60, K=50))])
+def test_iwae_parity(torch_cuda, name, kw):
+    """NEXT-3: tmc_iwae vs the oracle's IWAE (value and every input gradient), dlogp weights."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload(name, **kw)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B)
+    dl = np.linspace(-0.5, 1.5, wl.B)
+    logp, gr = tmc.iwae(g, upload(torch, wl), dlogp=torch.from_numpy(dl).cuda())
+    torch.cuda.synchronize()
+    ref = oracle.iwae(wl.parent, wl.K, wl.D, wl.z, wl.mu, wl.logvar, wl.logq, wl.logobs, dlogp=dl)
+    got = {"logp": logp.cpu().numpy()}
+    for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
+        got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
+    compare(got, ref, tag="iwae-" + name)

@@ -427,3 +427,80 @@ def test_sample_normal_distribution_and_keying():
     assert not np.array_equal(d9[:, 1, :8], d8[:, 1])
     other = oracle.sample_normal(8, 4, 10, 0, 1, 33, 5)
     assert not np.any(other == full)
+
+
+# ----------------------------------------------------------------------------- NEXT-3: IWAE
+def _iwae_wl(wl, **kw):
+    return oracle.iwae(wl.parent, wl.K, wl.D, wl.z, wl.mu, wl.logvar, wl.logq, wl.logobs, **kw)
+
+
+@pytest.mark.parametrize("name", TINY)
+def test_iwae_equals_diagonal_bruteforce(name):
+    """IWAE = log mean over the K diagonal index tuples of the brute-force weights."""
+    from bruteforce import iwae_bruteforce
+    wl = tw.make_workload(name)
+    r = _iwae_wl(wl, grads=False)
+    for b in range(wl.B):
+        fac, obs = workload_datapoint(wl, b)
+        assert abs(r["logp"][b] - iwae_bruteforce(wl.parent, wl.K, fac, obs)) <= 1e-10
+
+
+def test_iwae_K1_equals_tmc_K1():
+    """With one sample per latent IWAE and TMC are both the single-sample ELBO estimator."""
+    wl = tw.make_workload("C0", K=1)
+    a = _iwae_wl(wl, grads=False)["logp"]
+    b = oracle.estimate_workload(wl, grads=False)["logp"]
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["S_chain", "S_tree", "S_mlp"])
+def test_iwae_gradients_match_finite_differences(name):
+    """Oracle IWAE gradients vs central differences of the brute-force diagonal value (scipy)."""
+    from bruteforce import iwae_bruteforce, log_factor
+    wl = tw.make_workload(name)
+    r = _iwae_wl(wl, dlogp=np.ones(wl.B))
+    rng = np.random.default_rng(5)
+    b = 1
+    h = 1e-3
+
+    def value(zz, mm, vv):
+        fac = [log_factor(zz[i], mm[i], vv[i], wl.logq[i][b]) for i in range(len(wl.parent))]
+        obs = [None if wl.logobs[i] is None else wl.logobs[i][b].astype(np.float64) for i in range(len(wl.parent))]
+        return iwae_bruteforce(wl.parent, wl.K, fac, obs)
+    base = [[x[b].astype(np.float64) for x in arrs] for arrs in (wl.z, wl.mu, wl.logvar)]
+    for which, key in ((0, "dz"), (1, "dmu"), (2, "dlogvar")):
+        for _ in range(4):
+            i = int(rng.integers(len(wl.parent)))
+            arr = base[which][i]
+            idx = tuple(int(rng.integers(s)) for s in arr.shape)
+            vals = []
+            for sgn in (1, -1):
+                mod = [[a.copy() for a in lst] for lst in base]
+                mod[which][i][idx] += sgn * h
+                vals.append(value(*mod))
+            fd = (vals[0] - vals[1]) / (2 * h)
+            assert abs(fd - r[key][i][b][idx]) <= 1e-6 * max(1.0, abs(fd)), (key, i, idx, fd, r[key][i][b][idx])
+
+
+def test_iwae_unbiased_C0_closed_form():
+    """E[exp L_IWAE] = p(x) on C0's closed-form evidence, by Monte Carlo."""
+    wl = tw.make_workload("C0")
+    p = wl.params
+    S = np.eye(2)
+    for i in range(1, 4):
+        S = p["W"][i] @ S @ p["W"][i].T + 0.5 * np.eye(2)
+    cov = p["C"][3] @ S @ p["C"][3].T + 0.1 * np.eye(4)
+    R, K = 100_000, 8
+    b = 2
+    x = wl.x[b][0]
+    logpx = multivariate_normal.logpdf(x, np.zeros(4), cov)
+    rng = np.random.default_rng([31, b])
+    z = [rng.normal(0, math.sqrt(2), (R, K, 2)).astype(np.float32) for _ in range(4)]
+    lq = [norm.logpdf(zi.astype(np.float64), 0, math.sqrt(2)).sum(-1).astype(np.float32) for zi in z]
+    mu = [np.zeros((R, 1, 2), np.float32)] + [(z[i - 1].astype(np.float64) @ p["W"][i].T).astype(np.float32)
+                                               for i in range(1, 4)]
+    lv = [np.zeros((R, 1, 2), np.float32)] + [np.full((R, K, 2), math.log(0.5), np.float32) for _ in range(3)]
+    m = z[3].astype(np.float64) @ p["C"][3].T
+    lo = [None] * 3 + [(-0.5 * (((x - m) ** 2) / 0.1 + math.log(0.1) + math.log(2 * math.pi)).sum(-1)).astype(np.float32)]
+    logp = oracle.iwae([-1, 0, 1, 2], [K] * 4, [2] * 4, z, mu, lv, lq, lo, grads=False)["logp"]
+    _mc_check(logp, logpx, nsig=5.0)

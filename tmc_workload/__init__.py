@@ -111,6 +111,12 @@ CONFIGS: Dict[str, Config] = {
     "C4": Config("C4", "lg", B=256, K=512, parent=_tree_c4(), D=[32] * 21, w_var=1.0 / 32,
                  noise_var=0.3, observed=list(range(5, 21)), obs_dim=64, c_var=1.0 / 32,
                  obs_var=0.04, q="prior_marginal"),
+    # the paper's MNIST model shapes (4, 8, 16, 32, 64 stochastic
+    # units from the top layer to the layer next to the data; K = 20) on synthetic
+    # Bernoulli(0.13) pixels, with this family's 1-hidden-layer tanh conditionals (the paper's
+    # two leaky-relu deterministic layers and softplus stds are not reproduced: cost context only)
+    "M5": Config("M5", "mlp_chain", B=128, K=20, parent=_chain(5), D=[4, 8, 16, 32, 64], hidden=64,
+                 obs_kind="bernoulli", obs_dim=784, pixel_p=0.13),
     # the shared-parameter star of P:334-346 on toy 1: theta ~ N(0,1),
     # z_i | theta ~ N(theta, 1), x_i | z_i ~ N(z_i, 1), i = 1..N; proposals Q(theta) = N(0,1),
     # Q(z_i) = N(0,2).  One "datapoint" b is one whole data set of N points sharing theta
