@@ -9,7 +9,8 @@ from tmc_workload.torch_model import TorchModel
 
 
 @pytest.mark.parametrize("name,kw", [("S_mlp", {}), ("S_mlp_bern", {}), ("S_chain", {}), ("S_tree", {}),
-                                     ("C3", dict(B=2, K=8)), ("C4", dict(B=2, K=6))])
+                                     ("C3", dict(B=2, K=8)), ("C4", dict(B=2, K=6)), ("S_mnist", {}),
+                                     ("C1", dict(B=2, K=5)), ("M5", dict(B=2, K=4))])
 def test_torch_model_matches_workload(name, kw):
     wl = tw.make_workload(name, **kw)
     m = TorchModel(wl, "cpu")
@@ -24,8 +25,9 @@ def test_torch_model_matches_workload(name, kw):
             np.testing.assert_allclose(got.detach().numpy(), ref, rtol=2e-4, atol=2e-4, err_msg=f"{k}[{i}]")
 
 
-def test_torch_model_backward_accumulates_parameter_grads():
-    wl = tw.make_workload("S_mlp")
+@pytest.mark.parametrize("name", ["S_mlp", "S_mnist"])
+def test_torch_model_backward_accumulates_parameter_grads(name):
+    wl = tw.make_workload(name)
     m = TorchModel(wl, "cpu")
     f = m.forward()
     grads = [{k: (None if f[kk][i] is None else torch.ones_like(f[kk][i]))

@@ -10,7 +10,8 @@ plain torch (cuBLAS GEMMs) on the caller's device, built from the same parameter
 tmc_workload, so a bench "full step" can time model forward -> TMC -> model backward -> allreduce.
 It holds none of the TMC method's arithmetic (no factor, message, logsumexp or TMC gradient).
 
-Supported families: "mlp_chain" (C2, C3) and "lg" (C0, C4).
+Supported families: "mlp_chain" (C2, C3, M5), "lg" (C0, C4) and "mnist" (C1: amortised
+q(z1 | x), non-factorised q(z2 | z1^k) with diagonal pairing, A9).
 """
 from __future__ import annotations
 
@@ -27,8 +28,8 @@ class TorchModel:
         import torch
         self.torch = torch
         cfg = wl.cfg
-        if cfg.family not in ("mlp_chain", "lg"):
-            raise ValueError(f"torch harness supports mlp_chain / lg families, not {cfg.family}")
+        if cfg.family not in ("mlp_chain", "lg", "mnist"):
+            raise ValueError(f"torch harness supports mlp_chain / lg / mnist families, not {cfg.family}")
         self.cfg, self.device = cfg, device
         dt = dtype or torch.float32
         t = lambda a: torch.tensor(np.asarray(a), dtype=dt, device=device)
@@ -49,6 +50,25 @@ class TorchModel:
             # noise: eps = (z - mu_q) / sigma_q reproduces tmc_workload's samples
             self.eps = [t((wl.z[i].astype(np.float64) - p["q_mu"][i]) / p["q_sigma"][i]) for i in range(n)]
             self.x = t(np.stack([xs[0] for xs in wl.x]))
+        elif cfg.family == "mnist":
+            # latent 0 = z2 (top, prior N(0, I)), latent 1 = z1 (next to the data)
+            d2, d1 = D[0], D[1]
+            self.q_z1 = [(P(W), P(b)) for W, b in p["q_z1"]]
+            self.q_z2 = [(P(W), P(b)) for W, b in p["q_z2"]]
+            self.p_z1 = [(P(W), P(b)) for W, b in p["p_z1"]]
+            self.dec = [(P(W), P(b)) for W, b in p["dec"]]
+            self.x = t(np.stack([xs[0] for xs in wl.x]))
+            # noise that reproduces tmc_workload's samples: eps = (z - m_q) / s_q
+            f64 = lambda a: np.asarray(a, np.float64)
+            from tmc_workload import _mlp as mlp64
+            e1, e2 = [], []
+            for j in range(len(wl.b_ids)):
+                o = mlp64(p["q_z1"], f64(wl.x[j][0])[None, :])[0]
+                m1, s1 = o[:d1], np.exp(0.5 * o[d1:])
+                e1.append((f64(wl.z[1][j]) - m1) / s1)
+                o2 = mlp64(p["q_z2"], f64(wl.z[1][j]))
+                e2.append((f64(wl.z[0][j]) - o2[:, :d2]) / np.exp(0.5 * o2[:, d2:]))
+            self.eps = [t(np.stack(e2)), t(np.stack(e1))]
         else:
             self.W = [None] + [P(p["W"][i]) for i in range(1, n)]
             self.C = {i: P(c) for i, c in p["C"].items()}
@@ -67,7 +87,7 @@ class TorchModel:
         latent i, k), so every rank draws its own shard's noise and a datapoint's noise does not
         depend on the world size.  A training step calls this with a new seed each step."""
         import paper_1806_08593_b200 as tmc
-        if self.cfg.family != "mlp_chain":
+        if self.cfg.family not in ("mlp_chain", "mnist"):
             return                            # lg proposals are fixed samples (no reparameterisation)
         if self.b0 is None:
             raise ValueError("fresh_noise needs contiguous global datapoint ids")
@@ -117,6 +137,28 @@ class TorchModel:
             else:
                 var = cfg.obs_sigma ** 2
                 lo[n - 1] = (-0.5 * ((xb - out) ** 2 / var + math.log(var) + LOG2PI)).sum(-1)
+        elif cfg.family == "mnist":
+            d2, d1 = D[0], D[1]
+
+            def gauss(zv, m, lv, detach):
+                if detach:
+                    m, lv = m.detach(), lv.detach()
+                return (-0.5 * ((zv - m) ** 2 * torch.exp(-lv) + lv + LOG2PI)).sum(-1)
+            o = self._mlp(self.q_z1, self.x)                          # [B, 2 d1]
+            m1, lv1 = o[:, None, :d1], o[:, None, d1:]
+            z1 = m1 + torch.exp(0.5 * lv1) * self.eps[1]
+            o2 = self._mlp(self.q_z2, z1)                             # diagonal pairing (A9)
+            m2, lv2 = o2[..., :d2], o2[..., d2:]
+            z2 = m2 + torch.exp(0.5 * lv2) * self.eps[0]
+            z[0], z[1] = z2, z1
+            lq[1] = gauss(z1, m1, lv1, stl)
+            lq[0] = gauss(z2, m2, lv2, stl)
+            mu[0] = torch.zeros(B, 1, d2, device=self.device)
+            lv[0] = torch.zeros(B, 1, d2, device=self.device)
+            o3 = self._mlp(self.p_z1, z2)
+            mu[1], lv[1] = o3[..., :d1], o3[..., d1:]
+            logits = self._mlp(self.dec, z1)
+            lo[1] = (self.x[:, None, :] * logits - torch.nn.functional.softplus(logits)).sum(-1)
         else:
             for i in range(n):
                 z[i] = self.z_fixed[i]
@@ -149,7 +191,11 @@ class TorchModel:
 
     def proposal_params(self):
         """The recognition (proposal) parameters phi; everything else is generative (theta)."""
-        return list(self.q_mu) + list(self.q_logsig) if self.cfg.family == "mlp_chain" else []
+        if self.cfg.family == "mlp_chain":
+            return list(self.q_mu) + list(self.q_logsig)
+        if self.cfg.family == "mnist":
+            return [x for W, b in self.q_z1 + self.q_z2 for x in (W, b)]
+        return []
 
     def generative_params(self):
         ph = {id(p) for p in self.proposal_params()}
