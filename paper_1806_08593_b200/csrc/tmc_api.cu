@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -16,6 +17,7 @@
 #include "tmc_iwae.cuh"
 #include "tmc_sample.cuh"
 #include "tmc_simt.cuh"
+#include "tmc_small.cuh"
 #include "tmc_tc.cuh"
 
 namespace tmc {
@@ -38,6 +40,8 @@ struct EdgeBuf {
 
 struct Plan {
   int n = 0, B = 0, dir = 0, prec = 0;
+  int requested_prec = 0;          // the caller's tmc_precision (prec is the resolved path)
+  int requested_dir = 0;           // the caller's tmc_direction (dir is the resolved one)
   float alpha = 1.f;
   bool dense = false;
   std::vector<int> parent, K, D, Kp;
@@ -96,6 +100,8 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   p.dir = g->direction == TMC_DIR_AUTO ? (chain ? TMC_DIR_DOWN : TMC_DIR_UP) : g->direction;
   if (p.dir == TMC_DIR_DOWN && !chain) return fail(TMC_ERR_GRAPH, "TMC_DIR_DOWN requires a chain (parent[i] == i-1)");
   // precision
+  p.requested_prec = g->precision;
+  p.requested_dir = g->direction;
   p.prec = TMC_PREC_SIMT;
   if (!dense && g->precision != TMC_PREC_SIMT) {
     bool ok = tc_supported(p.parent, p.K, p.D);
@@ -338,6 +344,45 @@ tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* 
 }
 
 // ------------------------------------------------------------------------------------ forward
+// Small problems (K_i <= 64, D_i <= 128, n <= 32; TMC_PREC_AUTO and TMC_DIR_AUTO, Gaussian path):
+// one CTA per datapoint does the whole forward (mode 0) or forward + reverse (mode 1) in one
+// launch.  An explicit direction or precision selects the general kernels (the shared-root
+// exchange requires TMC_DIR_UP, so its backward never recomputes a shard-local forward here).
+bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in, const tmc_latent_grad* out,
+              double* logp, const double* dlogp, int mode) {
+  if (dense || p.requested_prec != TMC_PREC_AUTO || p.requested_dir != TMC_DIR_AUTO || p.n > small::kMaxN)
+    return false;
+  static const bool off = std::getenv("TMC_NO_SMALL") != nullptr;
+  if (off) return false;
+  for (int i = 0; i < p.n; ++i)
+    if (p.K[i] > small::kMaxK || p.Kp[i] > small::kMaxK || p.D[i] > small::kMaxD) return false;
+  if (!A) return true;
+  *A = small::Args{};
+  A->n = p.n; A->B = p.B; A->mode = mode; A->alpha = p.alpha; A->dlogp = dlogp; A->logp = logp;
+  for (int i = 0; i < p.n; ++i) {
+    small::Lat& L = A->l[i];
+    L.z = in[i].z; L.mu = in[i].mu; L.lv = in[i].logvar; L.logq = in[i].logq; L.logobs = in[i].logobs;
+    if (out) {
+      L.gz = out[i].dz; L.gmu = out[i].dmu; L.glv = out[i].dlogvar; L.gq = out[i].dlogq; L.go = out[i].dlogobs;
+      L.pair = out[i].pair_marginal;
+    }
+    L.K = p.K[i]; L.Kp = p.Kp[i]; L.D = p.D[i]; L.parent = p.parent[i];
+  }
+  return small::smem_bytes(*A) <= 160 * 1024;
+}
+
+tmc_status launch_small(const small::Args& A, cudaStream_t s) {
+  const size_t smem = small::smem_bytes(A);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(small::small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  small::small_kernel<<<A.B, small::kThreads, smem, s>>>(A);
+  TMC_COUNT_LAUNCH();
+  return launch_check("tmc (small-problem kernel)");
+}
+
 // phase: 0 = the whole forward; 1 = every latent below the (single) root, then the root's child
 // messages summed into xout [B][K_root+1] (fp64 residual sums, then the offset sum); 2 = the root's
 // elimination from h_root = u_root + xin (xin = the sum of phase-1 outputs over the shards of the
@@ -346,6 +391,10 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
                         void* ws, cudaStream_t s, int phase = 0, double* xout = nullptr,
                         const double* xin = nullptr) {
   if (p.B == 0) return TMC_OK;
+  if (phase == 0) {
+    small::Args A;
+    if (small_ok(p, dense != nullptr, &A, in, nullptr, logp, nullptr, 0)) return launch_small(A, s);
+  }
   // unary prep (all latents)
   if (phase != 2)
   for (int i0 = 0; i0 < p.n; i0 += kMaxUnaryPerLaunch) {
@@ -487,6 +536,11 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
 tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* const* dense, void* ws,
                          const double* dlogp, tmc_latent_grad* out, float* const* dlogf, cudaStream_t s) {
   if (p.B == 0) return TMC_OK;
+  {
+    // small problems: one launch that redoes the forward (logp into the workspace) and the reverse pass
+    small::Args A;
+    if (small_ok(p, dense != nullptr, &A, in, out, static_cast<double*>(ws), dlogp, 1)) return launch_small(A, s);
+  }
   std::vector<const float*> pi(p.n);
   auto grad = [&](int i) -> tmc_latent_grad { return out ? out[i] : tmc_latent_grad{}; };
   if (p.dir == TMC_DIR_DOWN) {

@@ -573,3 +573,33 @@ def test_iwae_parity(torch_cuda, name, kw):
     for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
         got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
     compare(got, ref, tag="iwae-" + name)
+
+
+@pytest.mark.parametrize("name,kw", [("C0", {}), ("C1", {}), ("S_tree", {}), ("S_hier", dict(N=31, K=64)),
+                                     ("C2", dict(B=3, K=16, D=[32, 64, 128, 64, 32]))])
+def test_small_problem_kernel(torch_cuda, name, kw):
+    """Small problems (K <= 64, D <= 128, n <= 32, TMC_PREC_AUTO) run as ONE launch per call
+    (C0/C1 are launch-bound): parity with the oracle, pair marginals included, and
+    exactly one kernel for tmc_forward and one for tmc_backward."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload(name, **kw)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B)
+    inp = upload(torch, wl)
+    ws = tmc.alloc_workspace(g)
+    logp = torch.empty(wl.B, dtype=torch.float64, device="cuda")
+    gr = tmc.alloc_grads(g, pair=True)
+    n0 = tmc.tmc_launch_count()
+    tmc.tmc_forward(g, inp, logp, ws)
+    n1 = tmc.tmc_launch_count()
+    dl = np.linspace(0.5, 1.5, wl.B)
+    tmc.tmc_backward(g, inp, ws, torch.from_numpy(dl).cuda(), gr)
+    n2 = tmc.tmc_launch_count()
+    torch.cuda.synchronize()
+    assert (n1 - n0, n2 - n1) == (1, 1)
+    ref = oracle.estimate_workload(wl, dlogp=dl, pair=True)
+    got = {"logp": logp.cpu().numpy()}
+    for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
+        got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
+    got["pair"] = [gr[i]["pair_marginal"].cpu().numpy() for i in range(len(wl.parent))]
+    compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag="small-" + name)
