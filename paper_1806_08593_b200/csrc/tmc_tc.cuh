@@ -798,6 +798,9 @@ struct BwdArgs {
 };
 
 template <int D>
+#ifndef TMC_BWD_NPOLY
+#define TMC_BWD_NPOLY 0   // reverse-pass softmax: groups (of 8) of 4 exponentials evaluated on the FMA pipe
+#endif
 #ifndef TMC_BWD_SPLIT
 #define TMC_BWD_SPLIT 1   // 1: S MMAs and gradient MMAs issued by two warps (see tc_bwd_kernel)
 #endif
@@ -919,6 +922,19 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
   // P~ == 0 everywhere, so every role skips it consistently (phase counters count live work only).
   auto olive = [](const BwdArgs& a, int b, int mt) -> bool { return !a.olive || a.olive[(size_t)b * a.o_tiles + mt]; };
   auto tlive = [](const BwdArgs& a, int b, int j) -> bool { return !a.tlive || a.tlive[(size_t)b * a.t_tiles + j]; };
+  // The streamed-tile flags of one datapoint as a register bitmask, loaded once per unit by a whole
+  // warp (a per-tile global load sat on every role's critical path: ~750 clk per tile).
+  auto tmask = [](const BwdArgs& a, int b) -> uint64_t {
+    if (!a.tlive) return ~0ull;
+    if (a.t_tiles > 64) return 0ull;                      // callers fall back to tlive()
+    const int l = threadIdx.x & 31;
+    const int f0 = l < a.t_tiles ? a.tlive[(size_t)b * a.t_tiles + l] : 0;
+    const int f1 = l + 32 < a.t_tiles ? a.tlive[(size_t)b * a.t_tiles + l + 32] : 0;
+    return (uint64_t)__ballot_sync(0xffffffffu, f0) | ((uint64_t)__ballot_sync(0xffffffffu, f1) << 32);
+  };
+  auto live = [&](const BwdArgs& a, int b, uint64_t msk, int j) -> bool {
+    return a.t_tiles <= 64 ? ((msk >> j) & 1ull) != 0 : tlive(a, b, j);
+  };
 #define TMC_BWD_UNIT()                                                   \
   const int e_ = batch_edge(fb, u);                                      \
   const BwdArgs& a = fb.e[e_];                                           \
@@ -1025,9 +1041,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
           TMC_BWD_UNIT();
           if (!olive(a, b, mt)) continue;
+          const uint64_t tm = tmask(a, b);
           int jj = 0;
           for (int j = 0; j < a.t_tiles; ++j) {
-            if (!tlive(a, b, j)) continue;
+            if (!live(a, b, tm, j)) continue;
             grad(a, t, jj == 0);
             ++jj;
             ++t;
@@ -1039,10 +1056,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         TMC_BWD_UNIT();
         if (!olive(a, b, mt)) continue;
+        const uint64_t tm = tmask(a, b);
         TMC_PROF_WAIT_M(6, mbar_wait(o_full, ua & 1));
         int jj = 0;                      // live streamed tiles so far in this unit
         for (int j = 0; j < a.t_tiles; ++j) {
-          if (!tlive(a, b, j)) continue;
+          if (!live(a, b, tm, j)) continue;
           const int s = t % ST, as = t % NSB;
           TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
           TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
@@ -1101,6 +1119,13 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
+#if defined(TMC_INSTRUMENT) && defined(TMC_SMX_PROF)
+    long long sprof[6] = {0, 0, 0, 0, 0, 0};   // waits, TMEM ld, math, TMEM st + release, unit start, row-sum handoff
+    long long _sp = clock64();
+#define TMC_SMX_MARK(q) do { const long long _n = clock64(); sprof[q] += _n - _sp; _sp = _n; } while (0)
+#else
+#define TMC_SMX_MARK(q) do {} while (0)
+#endif
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       TMC_BWD_UNIT();
       if (!olive(a, b, mt)) continue;
@@ -1108,13 +1133,16 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
       const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
       const float2 hom2 = make_float2(hom, hom);
       float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      TMC_SMX_MARK(4);
+      const uint64_t tm = tmask(a, b);
       for (int j = 0; j < a.t_tiles; ++j) {
-        if (!tlive(a, b, j)) continue;
+        if (!live(a, b, tm, j)) continue;
         if (SG == 2 && (int)(t & 1) != grp) { ++t; continue; }
         const int as = t % NSB, s = t % ST;
         TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
+        TMC_SMX_MARK(0);
 #pragma unroll 1
         for (int c = 0; c < (SG == 2 ? 2 : 1); ++c) {
           // column quarter handled now: 32 S columns; P~ hi/lo go back into the same 32 columns
@@ -1124,6 +1152,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
           if (!(a.dbg & 16)) {     // experiment flag 16: no TMEM traffic from the softmax warps
             TMC_LD32(taddr, v);
             tmem_ld_wait();
+            TMC_SMX_MARK(1);
           } else {
 #pragma unroll
             for (int q = 0; q < 32; ++q) v[q] = 0u;
@@ -1139,7 +1168,10 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
                                                        make_float2(h4.x, h4.y)), hom2);
               const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
                                                        make_float2(h4.z, h4.w)), hom2);
-              const float2 p01 = make_float2(ex2(y01.x), ex2(y01.y)), p23 = make_float2(ex2(y23.x), ex2(y23.y));
+              // the last TMC_BWD_NPOLY of the 8 groups of 4 exponentials run on the FMA pipe
+              const bool poly = q >= 8 - TMC_BWD_NPOLY;
+              const float2 p01 = poly ? make_float2(ex2_poly(y01.x), ex2_poly(y01.y)) : make_float2(ex2(y01.x), ex2(y01.y));
+              const float2 p23 = poly ? make_float2(ex2_poly(y23.x), ex2_poly(y23.y)) : make_float2(ex2(y23.x), ex2(y23.y));
               racc[0] = __fadd2_rn(racc[0], p01);
               racc[1] = __fadd2_rn(racc[1], p23);
               __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
@@ -1158,6 +1190,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
 #pragma unroll
             for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
           }
+          TMC_SMX_MARK(2);
           if (!(a.dbg & 16)) {
             TMC_ST16(taddr, hi);
             if constexpr (PLO) TMC_ST16(taddr + 16, lo);
@@ -1169,6 +1202,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
+        TMC_SMX_MARK(3);
         ++t;
       }
       // this warp's row sums -> the epilogue warps
@@ -1177,8 +1211,14 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
       sRs[(ua & 1) * 512 + (grp * 2 + slot) % 4 * 128 + m] = rr.x + rr.y;
       __syncwarp();
       if (lane == 0) mbar_arrive(&r_full[ua & 1]);
+      TMC_SMX_MARK(5);
       ++ua;
     }
+#if defined(TMC_INSTRUMENT) && defined(TMC_SMX_PROF)
+    if (lane == 0 && (sw == 0 || sw == 15))
+      for (int q = 0; q < 6; ++q) atomicAdd(&g_tmc_prof[blockIdx.x & 1023][19 + q + (sw ? 6 : 0)], (unsigned long long)sprof[q]);
+#endif
+#undef TMC_SMX_MARK
     TMC_PROF_END(lane == 0, 48 + sw, _tr2);
   } else {
     // ---------------- epilogue warps (4, one per TMEM lane quarter): G -> gradients, off the
@@ -1208,7 +1248,11 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
         continue;
       }
       int nl = 0;
-      for (int j = 0; j < a.t_tiles; ++j) nl += tlive(a, b, j) ? 1 : 0;
+      if (a.t_tiles <= 64) {
+        nl = __popcll(tmask(a, b) & (a.t_tiles == 64 ? ~0ull : ((1ull << a.t_tiles) - 1)));
+      } else {
+        for (int j = 0; j < a.t_tiles; ++j) nl += tlive(a, b, j) ? 1 : 0;
+      }
       const uint32_t gb = ua % GB;
       mbar_wait(&r_full[ua & 1], (ua >> 1) & 1);
       const float* rs = sRs + (ua & 1) * 512;
