@@ -891,11 +891,22 @@ tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, c
       }
       return roots;
     };
-    const unsigned grid = (unsigned)(((int64_t)p.B * K + 7) / 8);     // one warp per (b, k) row
+    bool vec4 = true;                                                 // every D % 4 == 0: float4 kernels
+    for (int i = 0; i < p.n; ++i) vec4 = vec4 && (p.D[i] % 4 == 0);
+    for (int i = 0; i < p.n && vec4; ++i)
+      for (const void* q : {(const void*)in[i].z, (const void*)in[i].mu, (const void*)in[i].logvar})
+        vec4 = vec4 && (reinterpret_cast<uintptr_t>(q) % 16 == 0);
+    if (out)
+      for (int i = 0; i < p.n && vec4; ++i)
+        for (const void* q : {(const void*)out[i].dz, (const void*)out[i].dmu, (const void*)out[i].dlogvar})
+          vec4 = vec4 && (reinterpret_cast<uintptr_t>(q) % 16 == 0);
+    const int64_t rows = (int64_t)p.B * K;
+    const unsigned grid = (unsigned)(vec4 ? (rows + 31) / 32 : (rows + 7) / 8);   // 4 or 1 rows per warp
     for (int i0 = 0; i0 < p.n; i0 += iwae::kMaxLat) {
       iwae::Batch bt;
       fill(i0, std::min(iwae::kMaxLat, p.n - i0), bt);
-      iwae::logw_kernel<<<grid, 256, 0, s>>>(bt, w, i0 == 0);
+      if (vec4) iwae::logw4_kernel<<<grid, 256, 0, s>>>(bt, w, i0 == 0);
+      else iwae::logw_kernel<<<grid, 256, 0, s>>>(bt, w, i0 == 0);
       TMC_COUNT_LAUNCH();
     }
     iwae::lse_kernel<<<p.B, 256, 0, s>>>(w, K, dlogp, logp);
@@ -904,10 +915,11 @@ tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, c
       for (int i0 = 0; i0 < p.n; i0 += iwae::kMaxLat) {
         iwae::Batch bt;
         const int roots = fill(i0, std::min(iwae::kMaxLat, p.n - i0), bt);
-        iwae::grad_kernel<<<grid, 256, 0, s>>>(bt, w);
+        if (vec4) iwae::grad4_kernel<<<grid, 256, 0, s>>>(bt, w);
+        else iwae::grad_kernel<<<grid, 256, 0, s>>>(bt, w);
         TMC_COUNT_LAUNCH();
         if (roots) {
-          iwae::root_grad_kernel<<<dim3(p.B, roots), 256, 0, s>>>(bt, w);
+          iwae::root_grad_kernel<<<dim3(p.B, roots), iwae::kRootWarps * 32, 0, s>>>(bt, w);
           TMC_COUNT_LAUNCH();
         }
       }
