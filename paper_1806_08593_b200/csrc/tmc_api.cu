@@ -190,6 +190,7 @@ void launch_pass_t(const PassArgs& a, cudaStream_t s) {
 template <bool ZR, int MODE>
 void launch_pass_m(const PassArgs& a, bool dense, cudaStream_t s) {
   if (dense) return launch_pass_t<ZR, MODE, true, 1>(a, s);
+  if (a.D == 1) return launch_pass_t<ZR, MODE, false, -1>(a, s);
   if (a.D <= 4) return launch_pass_t<ZR, MODE, false, 0>(a, s);
   if (a.D <= 32) return launch_pass_t<ZR, MODE, false, 1>(a, s);
   if (a.D <= 64) return launch_pass_t<ZR, MODE, false, 2>(a, s);
@@ -249,8 +250,9 @@ void launch_pass_batch_c(const std::vector<PassArgs>& v, cudaStream_t s) {
 template <int MODE>
 void launch_pass_batch_m(const std::vector<PassArgs>& as, bool dense, cudaStream_t s) {
   if (dense) return launch_pass_batch_c<MODE, true, 1>(as, s);
-  std::vector<PassArgs> cls[5];
-  for (const PassArgs& a : as) cls[a.D <= 4 ? 4 : a.D <= 32 ? 0 : a.D <= 64 ? 1 : a.D <= 128 ? 2 : 3].push_back(a);
+  std::vector<PassArgs> cls[6];
+  for (const PassArgs& a : as) cls[a.D == 1 ? 5 : a.D <= 4 ? 4 : a.D <= 32 ? 0 : a.D <= 64 ? 1 : a.D <= 128 ? 2 : 3].push_back(a);
+  launch_pass_batch_c<MODE, false, -1>(cls[5], s);
   launch_pass_batch_c<MODE, false, 0>(cls[4], s);
   launch_pass_batch_c<MODE, false, 1>(cls[0], s);
   launch_pass_batch_c<MODE, false, 2>(cls[1], s);

@@ -25,6 +25,8 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kOPW = 4;                  // owners per warp
 constexpr int kOPC = kOPW * kWarps;      // owners per CTA
 constexpr int kTC = 64;                  // streamed chunk
+constexpr int kTCSmall = 512;            // streamed chunk of the D <= 4 variant (no P buffer): the
+                                         // per-chunk staging latency is amortised over 8x the pairs
 
 __host__ __device__ inline int padded(int D) { return D | 1; }   // odd stride: conflict-free lanes
 
@@ -32,10 +34,12 @@ __host__ __device__ inline int padded(int D) { return D | 1; }   // odd stride: 
 __host__ inline size_t pass_smem_bytes(int D, bool dense) {
   if (dense) return sizeof(float) * (4 * kTC + 4 * kOPC + kWarps * kOPW * kTC + 32);
   int SD = padded(D);
-  size_t f = 2 * (size_t)kTC * SD + kTC      // streamed vectors (+beta)
+  const bool small = D <= 4;                 // pass_kernel<..., MAXDL = 0>
+  const size_t tck = small ? kTCSmall : kTC;
+  size_t f = 2 * tck * SD + tck              // streamed vectors (+beta)
            + 2 * (size_t)kOPC * SD + kOPC    // owner vectors (+beta)
-           + 2 * kTC + 2 * kOPC              // scalars
-           + (size_t)kWarps * kOPW * kTC     // P buffer
+           + 2 * tck + 2 * kOPC              // scalars
+           + (small ? 0 : (size_t)kWarps * kOPW * tck)   // P buffer
            + 32;
   return f * sizeof(float);
 }
@@ -69,26 +73,28 @@ __device__ __forceinline__ void pass_body(const PassArgs& a) {
   const int NS = OWNER_ROW ? a.C : a.R;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int obase = blockIdx.x * kOPC;
+  constexpr bool SMALL = (MAXDL <= 0);       // 0: D <= 4; -1: D == 1 exactly
+  constexpr int TCK = (SMALL && !DENSE) ? kTCSmall : kTC;
 
   extern __shared__ float sm[];
   float *sv0, *sv1, *sbeta, *ov0, *ov1, *obeta, *ss0, *ss1, *os0, *os1, *pbuf, *red;
   {
     float* p = sm;
     if (!DENSE) {
-      sv0 = p; p += kTC * SD;
-      sv1 = p; p += kTC * SD;
-      sbeta = p; p += kTC;
+      sv0 = p; p += TCK * SD;
+      sv1 = p; p += TCK * SD;
+      sbeta = p; p += TCK;
       ov0 = p; p += kOPC * SD;
       ov1 = p; p += kOPC * SD;
       obeta = p; p += kOPC;
     } else {
       p += 2 * kTC;  // keep layout simple
     }
-    ss0 = p; p += kTC;
-    ss1 = p; p += kTC;
+    ss0 = p; p += TCK;
+    ss1 = p; p += TCK;
     os0 = p; p += kOPC;
     os1 = p; p += kOPC;
-    pbuf = p; p += kWarps * kOPW * kTC;
+    pbuf = p; p += (SMALL && !DENSE) ? 0 : kWarps * kOPW * TCK;
     red = p;
   }
 
@@ -164,8 +170,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a) {
   // per-lane state.  SMALL (MAXDL == 0, D <= 4): each lane accumulates the owner-side Gaussian
   // gradient sums over its own streamed entries in phase 1 (warp-reduced in the epilogue) instead
   // of the lanes-over-dimensions phase 2, which would leave 31 of 32 lanes idle.
-  constexpr bool SMALL = (MAXDL == 0);
-  constexpr int NDL = SMALL ? 4 : MAXDL;
+  constexpr int NDL = (MAXDL == -1) ? 1 : (SMALL ? 4 : MAXDL);
   float lm[kOPW], ls[kOPW], ptot[kOPW];
   float acc0[kOPW][NDL], acc1[kOPW][NDL];
 #pragma unroll
@@ -175,8 +180,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a) {
     for (int q = 0; q < NDL; ++q) { acc0[j][q] = 0.f; acc1[j][q] = 0.f; }
   }
 
-  for (int s0 = 0; s0 < NS; s0 += kTC) {
-    const int tc = min(kTC, NS - s0);
+  for (int s0 = 0; s0 < NS; s0 += TCK) {
+    const int tc = min(TCK, NS - s0);
     __syncthreads();
     // ---- stage streamed chunk
     if (!DENSE) {
@@ -254,7 +259,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a) {
               }
             }
           } else {
-            pbuf[(warp * kOPW + j) * kTC + sl] = P;
+            pbuf[(warp * kOPW + j) * TCK + sl] = P;
           }
           ptot[j] += P;
           if (MODE == 1 && a.pair) a.pair[((int64_t)b * a.Kz + ai) * a.Kp + pi] = a.alpha * P;
@@ -268,7 +273,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a) {
       for (int j = 0; j < kOPW; ++j) {
         const int ol = warp * kOPW + j, o = obase + ol;
         if (o >= NO) continue;
-        const float* pw = pbuf + (warp * kOPW + j) * kTC;
+        const float* pw = pbuf + (warp * kOPW + j) * TCK;
 #pragma unroll
         for (int q = 0; q < MAXDL; ++q) {
           const int d = lane + 32 * q;
