@@ -65,3 +65,28 @@ def test_forward_statuses_without_gpu():
     if not torch.cuda.is_available():
         assert rc == -6                                            # TMC_ERR_UNSUPPORTED_DEVICE
         assert "device" in tmc.tmc_last_error()
+
+
+def test_extension_call_statuses_without_gpu():
+    """Argument validation of the calls added beyond the estimator happens before any device work."""
+    lib = tmc.load_library()
+    P = ctypes.c_void_p
+    fake = dict(z=4096, mu=4096, logvar=4096, logq=4096)
+    arr = tmc._inputs([fake, fake])
+    # IWAE needs equal K on every latent
+    g = tmc.Graph([-1, 0], [4, 5], [2, 2], B=2)
+    assert lib.tmc_iwae(g.ref(), arr, P(4096), None, None, P(4096), 1 << 20, None) == -2          # TMC_ERR_SHAPE
+    # the shared-root exchange needs an explicit UP direction and exactly one root
+    chain = tmc.Graph([-1, 0], [4, 4], [2, 2], B=2)
+    assert lib.tmc_forward_children(chain.ref(), arr, P(4096), P(4096), 1 << 30, None) == -3    # TMC_ERR_GRAPH
+    two_roots = tmc.Graph([-1, -1], [4, 4], [2, 2], B=2, direction=tmc.TMC_DIR_UP)
+    assert lib.tmc_forward_root(two_roots.ref(), arr, P(4096), P(4096), P(4096), 1 << 30, None) == -3
+    # sampler shapes
+    assert lib.tmc_sample_normal(0, 4, -1, 0, 0, 4, 4, P(4096), None) == -2
+    assert lib.tmc_sample_normal(0, 4, 2, 0, 0, 4, 0, P(4096), None) == -2
+    assert lib.tmc_sample_normal(0, 4, 0, 0, 0, 4, 4, None, None) == 0                            # empty: nothing to do
+    # host-streamed estimate: chunk must be positive
+    assert lib.tmc_estimate_host(chain.ref(), arr, P(4096), None, None, 0, P(4096), 1 << 30, None) == -1
+    assert lib.tmc_estimate_host_workspace_size(chain.ref(), 0) == 0
+    assert lib.tmc_estimate_host_workspace_size(chain.ref(), 1) > lib.tmc_workspace_size(
+        tmc.Graph([-1, 0], [4, 4], [2, 2], B=1).ref())
