@@ -877,10 +877,17 @@ struct BwdBatch {
 // SG = softmax groups: 1 = all 16 softmax warps on every tile (one 32-column quarter each);
 // 2 = two groups of 8 alternating tiles (each warp two 32-column quarters), so two tiles are in
 // the softmax stage at once and the S -> P~ -> gradient-GEMM handoffs of one group overlap the other.
+// SG: 1 = 16 softmax warps, one 32-column quarter each; 2 = two groups of 8 on alternating tiles;
+// 3 = 8 softmax warps, two column quarters each with both TMEM loads in flight together.
+__host__ __device__ constexpr int bwd_smw(int SG) { return SG == 3 ? 8 : 16; }
+template <int D, int SG>
+__host__ __device__ constexpr int bwd_threads() { return 32 * (bwd_smw(SG) + BGeo<D>::EW + 2 + TMC_BWD_SPLIT); }
+
 template <int D, int GT, int SG>
-__global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __grid_constant__ BwdBatch fb) {
+__global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const __grid_constant__ BwdBatch fb) {
   using G = BGeo<D>;
-  constexpr int ST = G::ST, SMW = G::SMW, EW = G::EW;
+  constexpr int ST = G::ST, SMW = bwd_smw(SG), EW = G::EW;
+  constexpr int SMX_ARRIVE = (SG == 2) ? SMW / 2 : SMW;     // softmax warps per tile
   constexpr int W_PROD = SMW + EW, W_MMA = SMW + EW + 1;     // role warps take the highest ids
   constexpr int W_MMAG = TMC_BWD_SPLIT ? W_MMA + 1 : W_MMA;  // gradient-MMA issuer (split mode)
   constexpr uint32_t IDESC_S = kIdescF16M128N128;
@@ -945,9 +952,9 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
     mbar_init(o_empty, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
-      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMW / SG);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMX_ARRIVE);
     }
-    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMW / SG); }
+    for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMX_ARRIVE); }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&g_full[s], 1); mbar_init(&g_empty[s], EW);
       mbar_init(&r_full[s], SMW); mbar_init(&r_empty[s], EW);
@@ -1115,7 +1122,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
     const int sw = warp;
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
     const int grp = (SG == 2) ? (sw >> 3) : 0;  // tile parity this warp processes (SG = 2)
-    const int slot = (SG == 2) ? ((sw >> 2) & 1) : (sw >> 2);   // row-sum slot (4 per row)
+    const int slot = (SG == 2) ? ((sw >> 2) & 1) : (SG == 3) ? (sw >> 2) * 2 : (sw >> 2);   // row-sum slot (4 per row)
     const int m = quarter * 32 + lane;          // owned row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0, ua = 0;
@@ -1126,6 +1133,34 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
 #else
 #define TMC_SMX_MARK(q) do {} while (0)
 #endif
+    // P~ of 32 columns: arguments S + ht + (ho + 14) on packed pairs, ex2, row-sum accumulation,
+    // fp16 hi/lo split
+    auto chunk_math = [&](const uint32_t* v, const float4* hts, float2 hom2, float2* racc, uint32_t* hi, uint32_t* lo) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 h4 = hts[q];
+        const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
+                                                 make_float2(h4.x, h4.y)), hom2);
+        const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
+                                                 make_float2(h4.z, h4.w)), hom2);
+        const bool poly = q >= 8 - TMC_BWD_NPOLY;
+        const float2 p01 = poly ? make_float2(ex2_poly(y01.x), ex2_poly(y01.y)) : make_float2(ex2(y01.x), ex2(y01.y));
+        const float2 p23 = poly ? make_float2(ex2_poly(y23.x), ex2_poly(y23.y)) : make_float2(ex2(y23.x), ex2(y23.y));
+        racc[0] = __fadd2_rn(racc[0], p01);
+        racc[1] = __fadd2_rn(racc[1], p23);
+        __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
+        hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
+        hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
+        if constexpr (PLO) {
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          const float2 d01 = __fadd2_rn(p01, make_float2(-f01.x, -f01.y));
+          const float2 d23 = __fadd2_rn(p23, make_float2(-f23.x, -f23.y));
+          __half2 l01 = __floats2half2_rn(d01.x, d01.y), l23 = __floats2half2_rn(d23.x, d23.y);
+          lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
+          lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
+        }
+      }
+    };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       TMC_BWD_UNIT();
       if (!olive(a, b, mt)) continue;
@@ -1143,6 +1178,26 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
         tc_fence_after();
         TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
         TMC_SMX_MARK(0);
+        if constexpr (SG == 3) {
+          // two column quarters, both TMEM loads in flight before the first wait
+          const int cq0 = (sw >> 2) * 2;
+          const uint32_t ta0 = tmem + lane_off + (uint32_t)(as * 128 + cq0 * 32), ta1 = ta0 + 32;
+          uint32_t v0[32], v1[32];
+          TMC_LD32(ta0, v0);
+          TMC_LD32(ta1, v1);
+          tmem_ld_wait();
+          TMC_SMX_MARK(1);
+          uint32_t hi[16], lo[16];
+          const float4* hts0 = reinterpret_cast<const float4*>(sHt + s * 128 + cq0 * 32);
+          if (hom > -INFINITY) chunk_math(v0, hts0, hom2, racc, hi, lo);
+          else for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
+          TMC_ST16(ta0, hi);
+          if constexpr (PLO) TMC_ST16(ta0 + 16, lo);
+          if (hom > -INFINITY) chunk_math(v1, hts0 + 8, hom2, racc, hi, lo);
+          TMC_SMX_MARK(2);
+          TMC_ST16(ta1, hi);
+          if constexpr (PLO) TMC_ST16(ta1 + 16, lo);
+        } else
 #pragma unroll 1
         for (int c = 0; c < (SG == 2 ? 2 : 1); ++c) {
           // column quarter handled now: 32 S columns; P~ hi/lo go back into the same 32 columns
@@ -1209,6 +1264,7 @@ __global__ void __launch_bounds__(BGeo<D>::THREADS, 1) tc_bwd_kernel(const __gri
       mbar_wait(&r_empty[ua & 1], ((ua >> 1) & 1) ^ 1);
       const float2 rr = __fadd2_rn(racc[0], racc[1]);
       sRs[(ua & 1) * 512 + (grp * 2 + slot) % 4 * 128 + m] = rr.x + rr.y;
+      if (SG == 3) sRs[(ua & 1) * 512 + (slot + 1) * 128 + m] = 0.f;
       __syncwarp();
       if (lane == 0) mbar_arrive(&r_full[ua & 1]);
       TMC_SMX_MARK(5);
@@ -1414,7 +1470,7 @@ inline bool tc_dense_reverse() {
 // Default number of fp16 terms of the reverse pass's gradient GEMM (TMC_BWD_GRAD_TERMS overrides).
 constexpr int kDefaultGradTerms = 3;
 // Default softmax grouping of the reverse pass (TMC_BWD_SG overrides).
-constexpr int kDefaultBwdGroups = 1;
+constexpr int kDefaultBwdGroups = 3;   // 8 softmax warps, two column quarters each (SG = 3)
 
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
@@ -1626,7 +1682,7 @@ inline int tc_grad_terms() {
 inline int tc_bwd_groups() {
   const char* e = std::getenv("TMC_BWD_SG");
   const int v = e ? std::atoi(e) : kDefaultBwdGroups;
-  return (v == 1 || v == 2) ? v : kDefaultBwdGroups;
+  return (v >= 1 && v <= 3) ? v : kDefaultBwdGroups;
 }
 
 template <int D, int GT, int SG>
@@ -1645,15 +1701,16 @@ inline void tc_bwd_launch_t(const tc::BwdBatch& fb, cudaStream_t s) {
   }
   const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
-  if (grid > 0) tc::tc_bwd_kernel<D, GT, SG><<<grid, G::THREADS, G::SMEM, s>>>(fb);
+  if (grid > 0) tc::tc_bwd_kernel<D, GT, SG><<<grid, tc::bwd_threads<D, SG>(), G::SMEM, s>>>(fb);
 }
 
 template <int D>
 inline void tc_bwd_launch(const tc::BwdBatch& fb, cudaStream_t s) {
-  const bool two = tc_bwd_groups() == 2;
+  const int sg = tc_bwd_groups();
   switch (tc_grad_terms()) {
-    case 4: return two ? tc_bwd_launch_t<D, 4, 2>(fb, s) : tc_bwd_launch_t<D, 4, 1>(fb, s);
-    default: return two ? tc_bwd_launch_t<D, 3, 2>(fb, s) : tc_bwd_launch_t<D, 3, 1>(fb, s);
+    case 4: return sg == 2 ? tc_bwd_launch_t<D, 4, 2>(fb, s) : tc_bwd_launch_t<D, 4, 1>(fb, s);
+    default: return sg == 2 ? tc_bwd_launch_t<D, 3, 2>(fb, s)
+                   : sg == 3 ? tc_bwd_launch_t<D, 3, 3>(fb, s) : tc_bwd_launch_t<D, 3, 1>(fb, s);
   }
 }
 
