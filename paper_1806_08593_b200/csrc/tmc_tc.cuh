@@ -879,6 +879,8 @@ struct BwdBatch {
 // the softmax stage at once and the S -> P~ -> gradient-GEMM handoffs of one group overlap the other.
 // SG: 1 = 16 softmax warps, one 32-column quarter each; 2 = two groups of 8 on alternating tiles;
 // 3 = 8 softmax warps, two column quarters each with both TMEM loads in flight together.
+// (4 softmax warps with all four quarters, loads in two pairs, measured 34% slower: one warp per
+// SMSP cannot keep the MUFU fed.)
 __host__ __device__ constexpr int bwd_smw(int SG) { return SG == 3 ? 8 : 16; }
 template <int D, int SG>
 __host__ __device__ constexpr int bwd_threads() { return 32 * (bwd_smw(SG) + BGeo<D>::EW + 2 + TMC_BWD_SPLIT); }
