@@ -51,6 +51,13 @@ struct Plan {
   std::vector<size_t> u, uoff;
   size_t zero = 0, lse = 0, flag = 0;
   std::vector<TcLatentBuf> tc;   // tensor-core operand buffers (per latent), empty for SIMT
+  // Tensor-core padding: a non-root latent whose D is not 32/64 (D < 64) is run on the D' = 32/64
+  // tensor-core path from zero-padded copies of its inputs in the workspace (padded dims: z = mu = 0,
+  // logvar = -ln 2 pi, so each contributes log N(0; 0, 1/(2 pi)) = 0 exactly to every pair), and its
+  // gradients are copied back unpadded.  Din = the caller's D; D = the internal (padded) one.
+  std::vector<int> Din;
+  std::vector<size_t> pz, pmu, plv, pgz, pgmu, pglv;
+  bool any_pad = false;
   size_t total = 0;
 };
 
@@ -82,6 +89,7 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   p.parent.assign(g->parent, g->parent + g->n);
   p.K.assign(g->K, g->K + g->n);
   p.D.assign(g->D, g->D + g->n);
+  p.Din = p.D;
   p.children.assign(p.n, {});
   for (int i = 0; i < p.n; ++i) {
     if (p.K[i] <= 0) return fail(TMC_ERR_SHAPE, "K[" + std::to_string(i) + "] must be >= 1");
@@ -99,6 +107,14 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   const bool chain = is_chain(p.parent);
   p.dir = g->direction == TMC_DIR_AUTO ? (chain ? TMC_DIR_DOWN : TMC_DIR_UP) : g->direction;
   if (p.dir == TMC_DIR_DOWN && !chain) return fail(TMC_ERR_GRAPH, "TMC_DIR_DOWN requires a chain (parent[i] == i-1)");
+  // tensor-core padding of small / odd D (large K only under AUTO; any K when TC is requested)
+  if (!dense && g->precision != TMC_PREC_SIMT)
+    for (int i = 0; i < p.n; ++i)
+      if (p.parent[i] >= 0 && p.D[i] < 64 && p.D[i] != 32 &&
+          (g->precision == TMC_PREC_TC || (p.K[i] >= 128 && p.Kp[i] >= 128))) {
+        p.D[i] = p.D[i] < 32 ? 32 : 64;
+        p.any_pad = true;
+      }
   // precision
   p.requested_prec = g->precision;
   p.requested_dir = g->direction;
@@ -106,7 +122,7 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   if (!dense && g->precision != TMC_PREC_SIMT) {
     bool ok = tc_supported(p.parent, p.K, p.D);
     if (g->precision == TMC_PREC_TC && !ok)
-      return fail(TMC_ERR_SHAPE, "TMC_PREC_TC needs D_i in {16,32,48,64} on every latent and K >= 1");
+      return fail(TMC_ERR_SHAPE, "TMC_PREC_TC needs D_i <= 64 on some non-root latent");
     if (ok) p.prec = TMC_PREC_TC;
   }
 
@@ -138,6 +154,16 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   p.lse = carve(cur, 4 * B);
   p.flag = carve(cur, 16);
   if (p.prec == TMC_PREC_TC) tc_plan(p.parent, p.K, p.D, p.Kp, p.B, p.dir, cur, p.tc);
+  p.pz.assign(p.n, 0); p.pmu.assign(p.n, 0); p.plv.assign(p.n, 0);
+  p.pgz.assign(p.n, 0); p.pgmu.assign(p.n, 0); p.pglv.assign(p.n, 0);
+  if (p.prec == TMC_PREC_TC)
+    for (int i = 0; i < p.n; ++i)
+      if (p.D[i] != p.Din[i]) {
+        const size_t zk = 4 * B * p.K[i] * p.D[i], mk = 4 * B * p.Kp[i] * p.D[i];
+        p.pz[i] = carve(cur, zk); p.pmu[i] = carve(cur, mk); p.plv[i] = carve(cur, mk);
+        p.pgz[i] = carve(cur, zk); p.pgmu[i] = carve(cur, mk); p.pglv[i] = carve(cur, mk);
+      }
+  if (p.prec != TMC_PREC_TC) { p.D = p.Din; p.any_pad = false; }   // padding only serves the TC path
   p.total = (cur + 255) & ~size_t(255);
   return TMC_OK;
 }
@@ -310,7 +336,7 @@ tmc_status check_inputs(const Plan& p, const tmc_latent_in* in, const float* con
     }
     if (!in[i].z || !in[i].mu || !in[i].logvar || !in[i].logq)
       return fail(TMC_ERR_INVALID_ARG, "latent " + std::to_string(i) + ": z/mu/logvar/logq must be non-NULL");
-    if (p.prec == TMC_PREC_TC) {
+    if (p.prec == TMC_PREC_TC && p.D[i] == p.Din[i]) {      // padded latents are copied (no alignment need)
       for (const void* q : {(const void*)in[i].z, (const void*)in[i].mu, (const void*)in[i].logvar})
         if (reinterpret_cast<uintptr_t>(q) % 16)
           return fail(TMC_ERR_ALIGNMENT, "tensor-core path needs 16-byte aligned z/mu/logvar");
@@ -331,9 +357,9 @@ tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* 
   for (int i = 0; i < p.n; ++i) {
     if (dense) { scan(dense[i], B * p.K[i] * p.Kp[i], 1); }
     else {
-      scan(in[i].z, B * p.K[i] * p.D[i], 0);
-      scan(in[i].mu, B * p.Kp[i] * p.D[i], 0);
-      scan(in[i].logvar, B * p.Kp[i] * p.D[i], 0);
+      scan(in[i].z, B * p.K[i] * p.Din[i], 0);
+      scan(in[i].mu, B * p.Kp[i] * p.Din[i], 0);
+      scan(in[i].logvar, B * p.Kp[i] * p.Din[i], 0);
       scan(in[i].logq, B * p.K[i], 1);
     }
     if (in && in[i].logobs) scan(in[i].logobs, B * p.K[i], 1);
@@ -343,6 +369,72 @@ tmc_status validate_inputs(const Plan& p, const tmc_latent_in* in, const float* 
   if (cudaStreamSynchronize(s) != cudaSuccess) return launch_check("validate");
   if (host) return fail(TMC_ERR_NONFINITE, "NaN or +inf (or -inf in z/mu/logvar) found in an input");
   return TMC_OK;
+}
+
+// ------------------------------------------------------------------------------- padding
+bool padded(const Plan& p, int i) { return p.prec == TMC_PREC_TC && p.D[i] != p.Din[i]; }
+
+void launch_pad(const std::vector<simt::PadDesc>& jobs, int unpad, cudaStream_t s) {
+  for (size_t j0 = 0; j0 < jobs.size(); j0 += simt::kMaxPad) {
+    simt::PadBatch pb{};
+    pb.count = (int)std::min<size_t>(simt::kMaxPad, jobs.size() - j0);
+    int64_t mx = 1;
+    for (int k = 0; k < pb.count; ++k) {
+      pb.d[k] = jobs[j0 + k];
+      mx = std::max<int64_t>(mx, pb.d[k].rows * (unpad ? pb.d[k].Di : pb.d[k].Dt));
+    }
+    const unsigned gx = (unsigned)std::min<int64_t>((mx + 255) / 256, 1024);
+    simt::pad_batch_kernel<<<dim3(gx, pb.count), 256, 0, s>>>(pb, unpad);
+    TMC_COUNT_LAUNCH();
+  }
+}
+
+// The inputs the kernels see: padded latents point at their workspace copies (filled when
+// `fill`, i.e. on the forward; the reverse pass reuses the forward's copies).
+std::vector<tmc_latent_in> kernel_inputs(const Plan& p, const tmc_latent_in* in, void* ws, cudaStream_t s, bool fill) {
+  std::vector<tmc_latent_in> v(in, in + p.n);
+  if (!p.any_pad) return v;
+  std::vector<simt::PadDesc> jobs;
+  for (int i = 0; i < p.n; ++i) {
+    if (!padded(p, i)) continue;
+    float* z = at<float>(ws, p.pz[i]);
+    float* mu = at<float>(ws, p.pmu[i]);
+    float* lv = at<float>(ws, p.plv[i]);
+    const int64_t rz = (int64_t)p.B * p.K[i], rm = (int64_t)p.B * p.Kp[i];
+    jobs.push_back({in[i].z, z, rz, p.Din[i], p.D[i], 0.f});
+    jobs.push_back({in[i].mu, mu, rm, p.Din[i], p.D[i], 0.f});
+    jobs.push_back({in[i].logvar, lv, rm, p.Din[i], p.D[i], -1.8378770664093453f});   // -ln(2 pi): adds exactly 0
+    v[i].z = z; v[i].mu = mu; v[i].logvar = lv;
+  }
+  if (fill && p.B > 0) launch_pad(jobs, 0, s);
+  return v;
+}
+
+// Gradient outputs the kernels write: padded latents write into workspace buffers (copied back
+// unpadded by unpad_outputs).
+std::vector<tmc_latent_grad> kernel_outputs(const Plan& p, const tmc_latent_grad* out, void* ws) {
+  std::vector<tmc_latent_grad> v(p.n);
+  for (int i = 0; i < p.n; ++i) {
+    v[i] = out ? out[i] : tmc_latent_grad{};
+    if (!out || !padded(p, i)) continue;
+    if (out[i].dz) v[i].dz = at<float>(ws, p.pgz[i]);
+    if (out[i].dmu) v[i].dmu = at<float>(ws, p.pgmu[i]);
+    if (out[i].dlogvar) v[i].dlogvar = at<float>(ws, p.pglv[i]);
+  }
+  return v;
+}
+
+void unpad_outputs(const Plan& p, const tmc_latent_grad* out, void* ws, cudaStream_t s) {
+  if (!out || !p.any_pad || p.B == 0) return;
+  std::vector<simt::PadDesc> jobs;
+  for (int i = 0; i < p.n; ++i) {
+    if (!padded(p, i)) continue;
+    const int64_t rz = (int64_t)p.B * p.K[i], rm = (int64_t)p.B * p.Kp[i];
+    if (out[i].dz) jobs.push_back({at<float>(ws, p.pgz[i]), out[i].dz, rz, p.Din[i], p.D[i], 0.f});
+    if (out[i].dmu) jobs.push_back({at<float>(ws, p.pgmu[i]), out[i].dmu, rm, p.Din[i], p.D[i], 0.f});
+    if (out[i].dlogvar) jobs.push_back({at<float>(ws, p.pglv[i]), out[i].dlogvar, rm, p.Din[i], p.D[i], 0.f});
+  }
+  launch_pad(jobs, 1, s);
 }
 
 // ------------------------------------------------------------------------------------ forward
@@ -730,12 +822,12 @@ tmc_status tmc_factors(const tmc_graph* g, int32_t i, const tmc_latent_in* in_i,
     if (p.B == 0) return TMC_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int Ki = p.K[i], Kp = p.Kp[i];
-    if (p.prec == TMC_PREC_TC && tc_factors_ok(Ki, Kp, p.D[i])) {
-      st = tc_factors(in_i, logf, p.B, Ki, Kp, p.D[i], s);
+    if (p.prec == TMC_PREC_TC && tc_factors_ok(Ki, Kp, p.Din[i])) {
+      st = tc_factors(in_i, logf, p.B, Ki, Kp, p.Din[i], s);
       if (st != TMC_OK) return st;
     } else {
       dim3 grid((Kp + 31) / 32, (Ki + 7) / 8, p.B);
-      simt::factors_kernel<<<grid, 256, 0, s>>>(in_i->z, in_i->mu, in_i->logvar, in_i->logq, logf, Ki, Kp, p.D[i]);
+      simt::factors_kernel<<<grid, 256, 0, s>>>(in_i->z, in_i->mu, in_i->logvar, in_i->logq, logf, Ki, Kp, p.Din[i]);
     TMC_COUNT_LAUNCH();
     }
     return launch_check("tmc_factors");
@@ -757,7 +849,9 @@ tmc_status tmc_forward(const tmc_graph* g, const tmc_latent_in* in, const float*
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (g->flags & TMC_FLAG_VALIDATE)
       if ((st = validate_inputs(p, in, logf_dense, ws, s)) != TMC_OK) return st;
-    return forward_impl(p, in, logf_dense, logp, ws, s);
+    if (logf_dense) return forward_impl(p, in, logf_dense, logp, ws, s);
+    const std::vector<tmc_latent_in> kin = kernel_inputs(p, in, ws, s, true);
+    return forward_impl(p, kin.data(), nullptr, logp, ws, s);
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }
@@ -773,7 +867,14 @@ tmc_status tmc_backward(const tmc_graph* g, const tmc_latent_in* in, const float
     if ((st = check_inputs(p, in, logf_dense)) != TMC_OK) return st;
     if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
     if ((st = check_device()) != TMC_OK) return st;
-    return backward_impl(p, in, logf_dense, ws, dlogp, out, dlogf_dense, reinterpret_cast<cudaStream_t>(stream));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (logf_dense) return backward_impl(p, in, logf_dense, ws, dlogp, out, dlogf_dense, s);
+    const std::vector<tmc_latent_in> kin = kernel_inputs(p, in, ws, s, false);
+    std::vector<tmc_latent_grad> kout = kernel_outputs(p, out, ws);
+    st = backward_impl(p, kin.data(), nullptr, ws, dlogp, out ? kout.data() : nullptr, nullptr, s);
+    if (st != TMC_OK) return st;
+    unpad_outputs(p, out, ws, s);
+    return launch_check("tmc_backward");
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }
@@ -809,7 +910,8 @@ tmc_status tmc_forward_children(const tmc_graph* g, const tmc_latent_in* in, dou
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (g->flags & TMC_FLAG_VALIDATE)
       if ((st = validate_inputs(p, in, nullptr, ws, s)) != TMC_OK) return st;
-    return forward_impl(p, in, nullptr, nullptr, ws, s, 1, root_msg, nullptr);
+    const std::vector<tmc_latent_in> kin = kernel_inputs(p, in, ws, s, true);
+    return forward_impl(p, kin.data(), nullptr, nullptr, ws, s, 1, root_msg, nullptr);
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }
@@ -822,7 +924,9 @@ tmc_status tmc_forward_root(const tmc_graph* g, const tmc_latent_in* in, const d
     tmc_status st = exchange_plan(g, in, ws, ws_bytes, p);
     if (st != TMC_OK) return st;
     if ((!root_msg_total || !logp) && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "root_msg_total / logp is NULL");
-    return forward_impl(p, in, nullptr, logp, ws, reinterpret_cast<cudaStream_t>(stream), 2, nullptr, root_msg_total);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const std::vector<tmc_latent_in> kin = kernel_inputs(p, in, ws, s, false);
+    return forward_impl(p, kin.data(), nullptr, logp, ws, s, 2, nullptr, root_msg_total);
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }
@@ -868,7 +972,7 @@ tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, c
     if (st != TMC_OK) return st;
     for (int i = 0; i < p.n; ++i) {
       if (p.K[i] != p.K[0]) return fail(TMC_ERR_SHAPE, "tmc_iwae needs equal K on every latent");
-      if (p.parent[i] < 0 && p.D[i] > 32 * iwae::kRootMaxChunks) return fail(TMC_ERR_SHAPE, "tmc_iwae: root D > 256");
+      if (p.parent[i] < 0 && p.Din[i] > 32 * iwae::kRootMaxChunks) return fail(TMC_ERR_SHAPE, "tmc_iwae: root D > 256");
     }
     if ((st = check_inputs(p, in, nullptr)) != TMC_OK) return st;
     if (p.B == 0) return TMC_OK;
@@ -888,13 +992,13 @@ tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, c
         iwae::LatDesc& L = bt.l[j];
         L.z = in[i].z; L.mu = in[i].mu; L.lv = in[i].logvar; L.logq = in[i].logq; L.logobs = in[i].logobs;
         if (out) { L.gz = out[i].dz; L.gmu = out[i].dmu; L.glv = out[i].dlogvar; L.gq = out[i].dlogq; L.go = out[i].dlogobs; }
-        L.D = p.D[i]; L.root = p.parent[i] < 0;
+        L.D = p.Din[i]; L.root = p.parent[i] < 0;
         roots += L.root;
       }
       return roots;
     };
     bool vec4 = true;                                                 // every D % 4 == 0: float4 kernels
-    for (int i = 0; i < p.n; ++i) vec4 = vec4 && (p.D[i] % 4 == 0);
+    for (int i = 0; i < p.n; ++i) vec4 = vec4 && (p.Din[i] % 4 == 0);
     for (int i = 0; i < p.n && vec4; ++i)
       for (const void* q : {(const void*)in[i].z, (const void*)in[i].mu, (const void*)in[i].logvar})
         vec4 = vec4 && (reinterpret_cast<uintptr_t>(q) % 16 == 0);
@@ -980,7 +1084,7 @@ tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double
       uint8_t* slot = w + (size_t)sl * L.slot_bytes;
       if (c >= 2) cudaStreamWaitEvent(hp->copy, hp->done[sl], 0);
       for (int i = 0; i < p.n; ++i) {
-        const size_t K = p.K[i], D = p.D[i], Kp = p.Kp[i];
+        const size_t K = p.K[i], D = p.Din[i], Kp = p.Kp[i];
         const size_t per[5] = {K * D, Kp * D, Kp * D, K, K};
         const float* src[5] = {in[i].z, in[i].mu, in[i].logvar, in[i].logq, in[i].logobs};
         float* dst[5];

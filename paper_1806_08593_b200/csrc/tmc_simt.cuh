@@ -444,6 +444,40 @@ __global__ void __launch_bounds__(256) hroot_kernel(const float* u, const double
   if (blockIdx.x == 0 && threadIdx.x == 0) hoff[b] = uoff[b] + x[(int64_t)b * (K + 1) + K];
 }
 
+// Tensor-core padding (tmc_api.cu): rows of Di floats -> rows of Dt floats (tail = fill), and back;
+// one launch per batch of up to kMaxPad arrays (blockIdx.y = array).
+constexpr int kMaxPad = 48;
+struct PadDesc { const float* src; float* dst; int64_t rows; int Di, Dt; float fill; };
+struct PadBatch { PadDesc d[kMaxPad]; int count; };
+__global__ void __launch_bounds__(256) pad_batch_kernel(const __grid_constant__ PadBatch pb, int unpad) {
+  const PadDesc& q = pb.d[blockIdx.y];
+  const int W = unpad ? q.Di : q.Dt;
+  const int64_t n = q.rows * W;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / W;
+    const int d = (int)(t - r * W);
+    if (unpad) q.dst[t] = q.src[r * q.Dt + d];
+    else q.dst[t] = d < q.Di ? q.src[r * q.Di + d] : q.fill;
+  }
+}
+__global__ void __launch_bounds__(256) pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                       int64_t rows, int Di, int Dt, float fill) {
+  const int64_t n = rows * Dt;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / Dt;
+    const int d = (int)(t - r * Dt);
+    dst[t] = d < Di ? src[r * Di + d] : fill;
+  }
+}
+__global__ void __launch_bounds__(256) unpad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                                         int64_t rows, int Di, int Dt) {
+  const int64_t n = rows * Di;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / Di;
+    dst[t] = src[r * Dt + (t - r * Di)];
+  }
+}
+
 // DOWN final: logp = off + LSE_a m[a] - ln K; save lse for the reverse pass.
 __global__ void __launch_bounds__(256) final_down_fwd_kernel(const float* m, const double* off, int K,
                                                              float lnK, float* lse, double* logp) {

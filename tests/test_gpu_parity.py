@@ -603,3 +603,18 @@ def test_small_problem_kernel(torch_cuda, name, kw):
         got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
     got["pair"] = [gr[i]["pair_marginal"].cpu().numpy() for i in range(len(wl.parent))]
     compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag="small-" + name)
+
+
+@pytest.mark.parametrize("name,kw,precision,direction", [
+    ("S_hier", dict(N=8, K=300, B=2), 0, 0),                       # D = 1, AUTO: padded to the D = 32 TC path
+    ("S_tree", dict(K=200, B=2, w_var=0.1), 2, 0),                 # D = 2,3,2,2,1 with TC requested
+    ("S_tree", dict(K=150, B=2, D=[48, 40, 8, 33, 20], w_var=1 / 48, c_var=1 / 48), 2, 0),   # pad to 64 and 32
+    ("C3", dict(B=2, K=130, D=[5] * 8), 2, 1),                     # DOWN chain, D = 5
+])
+def test_tensor_core_padding(torch_cuda, name, kw, precision, direction):
+    """Latents whose D is not 32/64 run on the tensor-core path from zero-padded copies (padded dims:
+    z = mu = 0, logvar = -ln 2 pi, contributing exactly 0); values and every gradient vs the oracle."""
+    wl = tw.make_workload(name, **kw)
+    got = run_gpu(torch_cuda, wl, precision=precision, direction=direction)
+    ref = oracle.estimate_workload(wl)
+    compare(got, ref, tag=f"pad-{name}")
