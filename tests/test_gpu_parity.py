@@ -618,3 +618,26 @@ def test_tensor_core_padding(torch_cuda, name, kw, precision, direction):
     got = run_gpu(torch_cuda, wl, precision=precision, direction=direction)
     ref = oracle.estimate_workload(wl)
     compare(got, ref, tag=f"pad-{name}")
+
+
+@pytest.mark.parametrize("name,kw", [("C3", dict(B=2, K=200)), ("S_hier", dict(N=4, K=150, B=2))])
+def test_validate_flag(torch_cuda, name, kw):
+    """TMC_FLAG_VALIDATE: NaN / +inf in an input -> TMC_ERR_NONFINITE before any compute; clean
+    inputs (including -inf in logobs, a legal probability-zero event) pass and match the oracle."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload(name, **kw)
+    last = len(wl.parent) - 1
+    wl.logobs[last][0, 3] = -np.inf
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, flags=tmc.TMC_FLAG_VALIDATE)
+    inp = upload(torch, wl)
+    logp, _ = tmc.estimate(g, inp, grads=False)
+    torch.cuda.synchronize()
+    ref = oracle.estimate_workload(wl, grads=False)
+    assert np.abs(logp.cpu().numpy() - ref["logp"]).max() <= LOGP_TOL
+    bad = [dict(d) for d in inp]
+    bad[1] = dict(bad[1], mu=bad[1]["mu"].clone())
+    bad[1]["mu"][0, 0, 0] = float("nan")
+    with pytest.raises(tmc.TmcError) as e:
+        tmc.estimate(g, bad, grads=False)
+    assert e.value.status == -8
