@@ -32,10 +32,11 @@ struct Args {
 __host__ inline size_t smem_bytes(const Args& a) {
   size_t d = 0, f = 0;
   int kk = 1, kp = 1;
+  auto r4 = [](size_t x) { return (x + 3) & ~size_t(3); };      // every fp32 array 16-byte aligned
   for (int i = 0; i < a.n; ++i) {
     const Lat& L = a.l[i];
     d += (size_t)L.K + L.Kp;
-    f += 3 * (size_t)L.K + (size_t)L.K * L.D + 2 * (size_t)L.Kp * L.D + L.Kp;   // pi, logq, logobs, z, mu, lam, ldet
+    f += 3 * r4(L.K) + r4((size_t)L.K * L.D) + 2 * r4((size_t)L.Kp * L.D) + r4(L.Kp);   // pi, logq, logobs, z, mu, lam, ldet
     kk = L.K > kk ? L.K : kk;
     kp = L.Kp > kp ? L.Kp : kp;
   }
@@ -58,12 +59,26 @@ __device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
   const int D = L.D;
   for (int t = threadIdx.x; t < L.K * L.Kp; t += kThreads) {
     const int a = t / L.Kp, c = t - a * L.Kp;
-    float q = 0.f;
-    for (int d = 0; d < D; ++d) {
-      const float df = S.z[a * D + d] - S.mu[c * D + d];
-      q = fmaf(df * df, S.lam[c * D + d], q);
+    float q = 0.f, q2 = 0.f;
+    if ((D & 3) == 0) {                       // 16-byte shared-memory loads, two accumulators
+      const float4* z4 = reinterpret_cast<const float4*>(S.z + a * D);
+      const float4* m4 = reinterpret_cast<const float4*>(S.mu + c * D);
+      const float4* l4 = reinterpret_cast<const float4*>(S.lam + c * D);
+      for (int d = 0; d < (D >> 2); ++d) {
+        const float4 zz = z4[d], mm = m4[d], ll = l4[d];
+        const float d0 = zz.x - mm.x, d1 = zz.y - mm.y, d2 = zz.z - mm.z, d3 = zz.w - mm.w;
+        q = fmaf(d0 * d0, ll.x, q);
+        q2 = fmaf(d1 * d1, ll.y, q2);
+        q = fmaf(d2 * d2, ll.z, q);
+        q2 = fmaf(d3 * d3, ll.w, q2);
+      }
+    } else {
+      for (int d = 0; d < D; ++d) {
+        const float df = S.z[a * D + d] - S.mu[c * D + d];
+        q = fmaf(df * df, S.lam[c * D + d], q);
+      }
     }
-    F[t] = alpha * (-0.5f * (q + S.ldet[c] + D * 1.8378770664093453f));
+    F[t] = alpha * (-0.5f * ((q + q2) + S.ldet[c] + D * 1.8378770664093453f));
   }
 }
 
@@ -74,18 +89,20 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   double* H[kMaxN];
   double* M[kMaxN];
   for (int i = 0; i < A.n; ++i) { H[i] = dp; dp += A.l[i].K; M[i] = dp; dp += A.l[i].Kp; }
+  if ((reinterpret_cast<uintptr_t>(dp) & 15) != 0) ++dp;      // fp32 region 16-byte aligned (slack in smem_bytes)
   float* fp = reinterpret_cast<float*>(dp);
   float* PI[kMaxN];
   Staged ST[kMaxN];
+  auto r4 = [](int x) { return (x + 3) & ~3; };            // matches smem_bytes: 16-byte aligned arrays
   for (int i = 0; i < A.n; ++i) {
     const Lat& L = A.l[i];
-    PI[i] = fp; fp += L.K;
-    ST[i].lq = fp; fp += L.K;
-    ST[i].lo = fp; fp += L.K;
-    ST[i].z = fp; fp += L.K * L.D;
-    ST[i].mu = fp; fp += L.Kp * L.D;
-    ST[i].lam = fp; fp += L.Kp * L.D;
-    ST[i].ldet = fp; fp += L.Kp;
+    PI[i] = fp; fp += r4(L.K);
+    ST[i].lq = fp; fp += r4(L.K);
+    ST[i].lo = fp; fp += r4(L.K);
+    ST[i].z = fp; fp += r4(L.K * L.D);
+    ST[i].mu = fp; fp += r4(L.Kp * L.D);
+    ST[i].lam = fp; fp += r4(L.Kp * L.D);
+    ST[i].ldet = fp; fp += r4(L.Kp);
   }
   float* F = fp;
   // stage this datapoint's inputs once (all copies in flight together); later phases read shared memory
