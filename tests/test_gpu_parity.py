@@ -641,3 +641,48 @@ def test_validate_flag(torch_cuda, name, kw):
     with pytest.raises(tmc.TmcError) as e:
         tmc.estimate(g, bad, grads=False)
     assert e.value.status == -8
+
+
+@pytest.mark.parametrize("B,n,M", [(3, 5, 6), (2, 4, 200)])
+def test_exact_discrete_marginalisation_hmm(torch_cuda, B, n, M):
+    """P:650-659 on the GPU dense-factor path: K_i = M states, stratified samples, uniform Q -> the
+    TMC estimate is the exact log p(x) of the discrete chain (forward algorithm), gradients = pair
+    marginals vs the oracle."""
+    import paper_1806_08593_b200 as tmc
+    import discrete
+    torch = torch_cuda
+    logf, obs, pi, A, _ = discrete.hmm(B=B, n=n, M=M)
+    parent = [-1] + list(range(n - 1))
+    g = tmc.Graph(parent, [M] * n, [1] * n, B)
+    lf = [torch.from_numpy(x).cuda() for x in logf]
+    inp = [dict(logobs=torch.from_numpy(o).cuda()) for o in obs]
+    ws = tmc.alloc_workspace(g)
+    logp = torch.empty(B, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward(g, inp, logp, ws, logf_dense=lf)
+    dlf = [torch.empty_like(x) for x in lf]
+    gr = [dict(dlogobs=torch.empty(B, M, device="cuda")) for _ in range(n)]
+    tmc.tmc_backward(g, inp, ws, None, gr, logf_dense=lf, dlogf_dense=dlf)
+    torch.cuda.synchronize()
+    exact = discrete.hmm_forward_algorithm(logf, obs)
+    assert np.abs(logp.cpu().numpy() - exact).max() <= LOGP_TOL
+    ref = oracle.estimate(parent, [M] * n, [1] * n, None, None, None, None, obs, logf_dense=logf, pair=True)
+    got = {"logp": logp.cpu().numpy(), "pair": [x.cpu().numpy() for x in dlf],
+           "dlogobs": [x["dlogobs"].cpu().numpy() for x in gr]}
+    compare(got, ref, keys=("pair", "dlogobs"), tag="hmm")
+
+
+def test_exact_discrete_marginalisation_mixed(torch_cuda):
+    """enumerating a discrete z_1 (uniform Q, one sample per state) inside TMC equals TMC on
+    the model with z_1 marginalised out (GPU dense path vs the analytic reference)."""
+    import paper_1806_08593_b200 as tmc
+    import discrete
+    torch = torch_cuda
+    lf, ob, p = discrete.mixed(B=3, M=5, K=300)
+    g = tmc.Graph([-1, 0], [5, 300], [1, 1], 3)
+    inp = [dict(logobs=None), dict(logobs=torch.from_numpy(ob[1]).cuda())]
+    ws = tmc.alloc_workspace(g)
+    logp = torch.empty(3, dtype=torch.float64, device="cuda")
+    tmc.tmc_forward(g, inp, logp, ws, logf_dense=[torch.from_numpy(x).cuda() for x in lf])
+    torch.cuda.synchronize()
+    ref = discrete.mixed_marginalised_reference(lf, ob, 300)
+    assert np.abs(logp.cpu().numpy() - ref).max() <= LOGP_TOL

@@ -504,3 +504,19 @@ def test_iwae_unbiased_C0_closed_form():
     lo = [None] * 3 + [(-0.5 * (((x - m) ** 2) / 0.1 + math.log(0.1) + math.log(2 * math.pi)).sum(-1)).astype(np.float32)]
     logp = oracle.iwae([-1, 0, 1, 2], [K] * 4, [2] * 4, z, mu, lv, lq, lo, grads=False)["logp"]
     _mc_check(logp, logpx, nsig=5.0)
+
+
+# ----------------------------------------------------------------------------- exact discrete marginalisation
+def test_oracle_dense_path_exact_discrete_marginalisation():
+    """with K_i = number of states, stratified samples and uniform Q, the TMC estimate of
+    an all-discrete chain IS log p(x) (the forward algorithm), and enumerating a discrete z_1 in a
+    mixed model equals TMC on the model with z_1 marginalised out."""
+    import discrete
+    logf, obs, pi, A, _ = discrete.hmm(B=3, n=5, M=6)
+    n, M = 5, 6
+    r = oracle.estimate([-1] + list(range(n - 1)), [M] * n, [1] * n, None, None, None, None, obs,
+                        logf_dense=logf, grads=False)
+    np.testing.assert_allclose(r["logp"], discrete.hmm_forward_algorithm(logf, obs), rtol=0, atol=1e-9)
+    lf, ob, p = discrete.mixed(B=3, M=4, K=7)
+    r = oracle.estimate([-1, 0], [4, 7], [1, 1], None, None, None, None, ob, logf_dense=lf, grads=False)
+    np.testing.assert_allclose(r["logp"], discrete.mixed_marginalised_reference(lf, ob, 7), rtol=0, atol=1e-9)
