@@ -686,3 +686,15 @@ def test_exact_discrete_marginalisation_mixed(torch_cuda):
     torch.cuda.synchronize()
     ref = discrete.mixed_marginalised_reference(lf, ob, 300)
     assert np.abs(logp.cpu().numpy() - ref).max() <= LOGP_TOL
+
+
+@pytest.mark.parametrize("name,kw", [("S_tree", {}), ("C4", dict(B=2, K=130)), ("C3", dict(B=2, K=200))])
+def test_pair_marginal_invariants(torch_cuda, name, kw):
+    """with dlogp = 1 every edge's pair marginals sum to 1, and the row sums of P_i
+    equal pi_i = dlogobs_i (the marginal of k_i), per datapoint."""
+    wl = tw.make_workload(name, **kw)
+    got = run_gpu(torch_cuda, wl, pair=True)
+    for i in range(len(wl.parent)):
+        P = got["pair"][i].astype(np.float64)
+        np.testing.assert_allclose(P.sum(axis=(1, 2)), 1.0, rtol=0, atol=1e-4)
+        np.testing.assert_allclose(P.sum(axis=2), got["dlogobs"][i], rtol=1e-4, atol=1e-6)   # two passes, fp32
