@@ -203,11 +203,8 @@ void launch_pass_t(const PassArgs& a, cudaStream_t s) {
   const int NO = (MODE != 2) ? a.R : a.C;
   const size_t smem = simt::pass_smem_bytes(a.D, DENSE);
   auto kern = simt::pass_kernel<ZR, MODE, DENSE, MAXDL>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(kern, 200 * 1024, attr);
   dim3 grid((NO + simt::kOPC - 1) / simt::kOPC, a.B);
   kern<<<grid, simt::kThreads, smem, s>>>(a);
     TMC_COUNT_LAUNCH();
@@ -248,11 +245,8 @@ void launch_pass(const PassArgs& a, bool zrows, int mode, bool dense, cudaStream
 template <bool ZR, int MODE, bool DENSE, int MAXDL>
 void launch_pass_batch_t(const PassArgs* as, int ne, cudaStream_t s) {
   auto kern = simt::pass_batch_kernel<ZR, MODE, DENSE, MAXDL>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(kern, 200 * 1024, attr);
   for (int e0 = 0; e0 < ne; e0 += simt::kMaxPassBatch) {
     simt::PassBatch pb{};
     const int n = std::min(simt::kMaxPassBatch, ne - e0);
@@ -467,11 +461,8 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
 
 tmc_status launch_small(const small::Args& A, cudaStream_t s) {
   const size_t smem = small::smem_bytes(A);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small::small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(small::small_kernel, 160 * 1024, attr);
   small::small_kernel<<<A.B, small::kThreads, smem, s>>>(A);
   TMC_COUNT_LAUNCH();
   return launch_check("tmc (small-problem kernel)");
@@ -944,12 +935,7 @@ tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0,
     if ((D & 3) == 0 && reinterpret_cast<uintptr_t>(eps) % 16)
       return fail(TMC_ERR_ALIGNMENT, "eps must be 16-byte aligned when D % 4 == 0");
     const int64_t n = (int64_t)B * K * ((D + 3) / 4);
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16);
     rng::normal_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(seed, tag, B, b0, latent, K, D, eps);
     TMC_COUNT_LAUNCH();

@@ -5,6 +5,29 @@
 
 namespace tmc {
 
+// Per-device one-time state (kernel attributes, SM counts): a process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+inline int sm_count() {
+  static int sms[kMaxDevices] = {};
+  const int d = current_device();
+  if (!sms[d]) cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, d);
+  return sms[d];
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel instantiation, device)
+template <typename Kernel>
+inline void ensure_smem_attr(Kernel k, int bytes, bool* done) {
+  const int d = current_device();
+  if (!done[d]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done[d] = true;
+  }
+}
+
 constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kLog2E = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

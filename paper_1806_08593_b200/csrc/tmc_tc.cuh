@@ -1594,17 +1594,9 @@ inline int tc_fwd_variant() {
 template <int D, int NPOLY, bool MF>
 inline void tc_fwd_launch_t(const tc::FwdBatch& fb, cudaStream_t s) {
   using G = tc::Geo<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::tc_fwd_kernel<D, NPOLY, MF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(tc::tc_fwd_kernel<D, NPOLY, MF>, (int)G::SMEM, attr);
+  const int sms = sm_count();
   const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
   if (grid > 0) tc::tc_fwd_kernel<D, NPOLY, MF><<<grid, G::THREADS, G::SMEM, s>>>(fb);
@@ -1690,17 +1682,9 @@ inline int tc_bwd_groups() {
 template <int D, int GT, int SG>
 inline void tc_bwd_launch_t(const tc::BwdBatch& fb, cudaStream_t s) {
   using G = tc::BGeo<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::tc_bwd_kernel<D, GT, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(tc::tc_bwd_kernel<D, GT, SG>, (int)G::SMEM, attr);
+  const int sms = sm_count();
   const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
   if (grid > 0) tc::tc_bwd_kernel<D, GT, SG><<<grid, tc::bwd_threads<D, SG>(), G::SMEM, s>>>(fb);
@@ -2054,17 +2038,9 @@ inline bool tc_factors_ok(int Ki, int Kp, int D) { return (D == 32 || D == 64) &
 template <int D>
 inline void tc_factors_launch(const tc::FacArgs& f, cudaStream_t s) {
   using G = tc::FGeo<D>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::tc_factors_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static bool attr[kMaxDevices] = {};
+  ensure_smem_attr(tc::tc_factors_kernel<D>, (int)G::SMEM, attr);
+  const int sms = sm_count();
   const int units = f.B * ((f.Kz + 127) / 128);
   const int grid = units < sms ? units : sms;
   tc::tc_factors_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(f);
