@@ -742,6 +742,7 @@ namespace {
 struct HostPipe {            // per device: the copy stream and slot events (created once, never freed)
   cudaStream_t copy = nullptr;
   cudaEvent_t start = nullptr, copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  std::mutex enqueue;        // calls from several host threads on one device enqueue one at a time
 };
 
 tmc_status host_pipe(HostPipe*& hp) {
@@ -1056,6 +1057,7 @@ tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double
     stage_layout(g, cb, pc.total, L);
     HostPipe* hp = nullptr;
     if ((st = host_pipe(hp)) != TMC_OK) return st;
+    std::lock_guard<std::mutex> lk(hp->enqueue);     // the slot events are shared per device
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     uint8_t* w = static_cast<uint8_t*>(ws);
     double* logp_dev = reinterpret_cast<double*>(w + 2 * L.slot_bytes);
