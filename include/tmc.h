@@ -209,7 +209,9 @@ tmc_status tmc_iwae(const tmc_graph *g, const tmc_latent_in *in, double *logp, c
  * (tag, b0 + b, latent, k * ceil(D/4) + d/4) gives the 4 words of dims 4j..4j+3; each word pair
  * (w0, w1) -> u = ((w >> 8) + 0.5) 2^-24 -> Box-Muller sqrt(-2 ln u0) (cos, sin)(2 pi u1), with ln,
  * cos and sin as fixed fp32 polynomials in correctly rounded fma/mul/add/div/sqrt (no libm), so a
- * host implementation performing the same operations reproduces every bit. */
+ * host implementation performing the same operations reproduces every bit.
+ * Limits: K * ceil(D/4) <= 2^31 - 1 and b0 + B <= 2^32 - 1 (32-bit counter words), else
+ * TMC_ERR_SHAPE. */
 tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0, int32_t latent, int32_t K,
                              int32_t D, float *eps, tmc_stream_t stream);
 

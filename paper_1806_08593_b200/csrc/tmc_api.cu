@@ -928,6 +928,8 @@ tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0,
                              float* eps, tmc_stream_t stream) {
   try {
     if (B < 0 || K < 0 || D <= 0 || b0 < 0 || latent < 0) return fail(TMC_ERR_SHAPE, "tmc_sample_normal: bad shape");
+    if ((int64_t)K * ((D + 3) / 4) > INT32_MAX || b0 + (int64_t)B > UINT32_MAX)
+      return fail(TMC_ERR_SHAPE, "tmc_sample_normal: K*ceil(D/4) and b0+B must fit the 32-bit counter words");
     if ((int64_t)B * K == 0) return TMC_OK;
     if (!eps) return fail(TMC_ERR_INVALID_ARG, "eps is NULL");
     if (reinterpret_cast<uintptr_t>(eps) % 4) return fail(TMC_ERR_ALIGNMENT, "eps must be 4-byte aligned");
