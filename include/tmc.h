@@ -33,7 +33,8 @@
  *   - Graph metadata (tmc_graph.parent/K/D, the pointer arrays themselves) are
  *     HOST memory.  Every float/double buffer is DEVICE memory owned by the
  *     caller, contiguous row-major, 4-byte aligned (16-byte for the tensor-core
- *     path, see TMC_PREC_TC).  The library allocates nothing.
+ *     path, see TMC_PREC_TC).  The library allocates no device memory
+ *     (tmc_estimate_host keeps one copy stream and five events per device).
  *   - Calls are asynchronous and stream-ordered on `stream`; they are reentrant
  *     across streams given distinct workspaces.  Shape/graph/argument errors
  *     are detected synchronously and nothing is launched.  Launch failures
@@ -76,7 +77,10 @@ typedef enum { TMC_DIR_AUTO = 0, TMC_DIR_DOWN = 1, TMC_DIR_UP = 2 } tmc_directio
 typedef enum {
   TMC_PREC_AUTO = 0, /* TC where the shape allows it, SIMT otherwise                         */
   TMC_PREC_SIMT = 1, /* fp32 CUDA-core direct form sum_d (z-mu)^2/s^2                        */
-  TMC_PREC_TC = 2    /* expanded quadratic form on tcgen05 tensor cores, 3-term fp16 split  */
+  TMC_PREC_TC = 2    /* expanded quadratic form on tcgen05 tensor cores, 3-term fp16 split; */
+                     /* a non-root latent with D not in {32,64} (D <= 64) runs from zero-    */
+                     /* padded workspace copies (padded dims contribute exactly 0); AUTO     */
+                     /* pads only when K_i, K_p >= 128                                       */
 } tmc_precision;
 
 enum { TMC_FLAG_VALIDATE = 1u };
