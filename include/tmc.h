@@ -75,7 +75,9 @@ typedef enum { TMC_DIR_AUTO = 0, TMC_DIR_DOWN = 1, TMC_DIR_UP = 2 } tmc_directio
 /* AUTO = DOWN for chains (parent[i] == i-1), UP otherwise. Both give the same logp. */
 
 typedef enum {
-  TMC_PREC_AUTO = 0, /* TC where the shape allows it, SIMT otherwise                         */
+  TMC_PREC_AUTO = 0, /* TC where the shape allows it, SIMT otherwise; small problems (all   */
+                     /* K_i <= 64, D_i <= 128, n <= 32, direction AUTO) run as one fused   */
+                     /* launch per tmc_forward / tmc_backward (one CTA per datapoint)      */
   TMC_PREC_SIMT = 1, /* fp32 CUDA-core direct form sum_d (z-mu)^2/s^2                        */
   TMC_PREC_TC = 2    /* expanded quadratic form on tcgen05 tensor cores, 3-term fp16 split; */
                      /* a non-root latent with D not in {32,64} (D <= 64) runs from zero-    */
