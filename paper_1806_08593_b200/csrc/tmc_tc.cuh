@@ -429,6 +429,27 @@ struct ColbiasArgs {
 
 struct ColbiasBatch { ColbiasArgs e[16]; int ne; };
 
+// Row r of a K=16 bias operand tile (the extra MMA that adds a per-column term to S): the value as
+// four fp16-representable parts (each within +-60000 log2 units), every part as fp16 hi + lo in
+// slots k = 2j, 2j+1 (the constant A operand has ones in k = 0..7); exact to ~2^-22 relative over
+// +-240000 log2 units (beyond that, a dead entry, clamped).
+__device__ __forceinline__ void store_bias_row(uint8_t* tiles, int r, float v) {
+  uint32_t w[4];
+  float rest = fminf(fmaxf(v, -240000.f), 240000.f);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float part = (j < 3) ? fminf(fmaxf(rest, -60000.f), 60000.f) : rest;
+    rest -= part;
+    __half hh, ll;
+    split16(part, hh, ll);
+    w[j] = (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
+  }
+  uint8_t* tile = tiles + (size_t)(r / kTileRows) * kBxBytes;
+  const int rr = r % kTileRows;
+  *reinterpret_cast<uint4*>(tile + bx_off(rr, 0)) = make_uint4(w[0], w[1], w[2], w[3]);
+  *reinterpret_cast<uint4*>(tile + bx_off(rr, 8)) = make_uint4(0u, 0u, 0u, 0u);
+}
+
 __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__ ColbiasBatch cbb_) {
   const ColbiasArgs& a = cbb_.e[blockIdx.y];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -460,24 +481,7 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__
     a.cb2[(size_t)b * a.Cpad + c] = v;
     if (v > -INFINITY) s_live[c / kTileRows] = 1;
     if (a.bx) {
-      // row c of the extra operand: the bias as four fp16-representable parts (each >= -60000 log2
-      // units), every part as fp16 hi + lo in slots k = 2j, 2j+1 (the constant A operand has ones in
-      // k = 0..7), so the tensor core adds the column bias to S to ~2^-22 relative over a range of
-      // 240000 log2 units below the column maximum (a dead column beyond that is clamped there).
-      uint32_t w[4];
-      float rest = fminf(fmaxf(v, -240000.f), 240000.f);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float part = (j < 3) ? fminf(fmaxf(rest, -60000.f), 60000.f) : rest;
-        rest -= part;
-        __half hh, ll;
-        split16(part, hh, ll);
-        w[j] = (uint32_t)__half_as_ushort(hh) | ((uint32_t)__half_as_ushort(ll) << 16);
-      }
-      uint8_t* tile = a.bx + ((size_t)b * (a.Cpad / kTileRows) + c / kTileRows) * kBxBytes;
-      const int r = c % kTileRows;
-      *reinterpret_cast<uint4*>(tile + bx_off(r, 0)) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4*>(tile + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
+      store_bias_row(a.bx + (size_t)b * (a.Cpad / kTileRows) * kBxBytes, c, v);
     }
   }
   __syncthreads();
@@ -785,6 +789,7 @@ struct BwdArgs {
   int o_tiles, t_tiles;
   const float* ho;             // [B][o_tiles*128] owned log2 term
   const float* ht;             // [B][t_tiles*128] streamed log2 term (-inf padded)
+  const uint8_t* Hx;           // [B][t_tiles][kBxBytes] the same term as the K=16 bias operand (added by the tensor core)
   const float* sgn;            // [B] signed scale of the upstream weights (w = sgn * |w|/|sgn|)
   float alpha;                 // factor power (param-side gradients scale by alpha; the Y tiles carry it already)
   int M, B;
@@ -812,7 +817,8 @@ struct BGeo {
   static constexpr int SMW = 16;                               // softmax warps (4 per TMEM lane quarter)
   static constexpr int EW = 4;                                 // epilogue warps (1 per TMEM lane quarter)
   static constexpr int THREADS = 32 * (SMW + EW + 2 + TMC_BWD_SPLIT);
-  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + ST * 512 + 2 * 4 * 128 * 4 + 512;
+  static constexpr size_t SMEM = 1024 + (size_t)TILE + (size_t)ST * TILE + (size_t)(ST + 1) * 4096 /*bias ring + ones*/ +
+                                 2 * 4 * 128 * 4 + 512;
 };
 
 // MN-major SWIZZLE_128B descriptor: LBO = stride of 64-element MN chunks, SBO = 8-row K groups.
@@ -907,8 +913,9 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sO = smem;
   uint8_t* sT = sO + G::TILE;
-  float* sHt = reinterpret_cast<float*>(sT + (size_t)ST * G::TILE);
-  float* sRs = sHt + ST * 128;                              // [2 (unit parity)][4 (column quarter)][128]
+  uint8_t* sHx = sT + (size_t)ST * G::TILE;                 // [ST] streamed-term bias operand tiles
+  uint8_t* sOnes = sHx + (size_t)ST * kBxBytes;             // constant ones A operand of the bias MMA
+  float* sRs = reinterpret_cast<float*>(sOnes + kBxBytes);  // [2 (unit parity)][4 (column quarter)][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRs + 1024);
   uint64_t* o_full = bars + 0;
   uint64_t* o_empty = bars + 1;
@@ -954,7 +961,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
     mbar_init(o_empty, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(&t_full[s], 1); mbar_init(&t_empty[s], 1);
-      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], SMX_ARRIVE);
+      mbar_init(&h_full[s], 1); mbar_init(&h_empty[s], 1);      // bias tile: read by the S MMAs only
     }
     for (int s = 0; s < NSB; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], 1); mbar_init(&p_full[s], SMX_ARRIVE); }
     for (int s = 0; s < 2; ++s) {
@@ -963,6 +970,11 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int r = tid; r < kTileRows; r += blockDim.x) {       // ones in k = 0..7 (times the bias parts)
+    *reinterpret_cast<uint4*>(sOnes + bx_off(r, 0)) = make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
+    *reinterpret_cast<uint4*>(sOnes + bx_off(r, 8)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async();
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -994,8 +1006,8 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
             bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, tb, &t_full[s]);
           }
           TMC_PROF_WAIT(true, 1, mbar_wait(&h_empty[s], ph));
-          mbar_expect_tx(&h_full[s], 512);
-          bulk_g2s(sHt + s * 128, a.ht + ((size_t)b * a.t_tiles + j) * 128, 512, &h_full[s]);
+          mbar_expect_tx(&h_full[s], kBxBytes);
+          bulk_g2s(sHx + (size_t)s * kBxBytes, a.Hx + ((size_t)b * a.t_tiles + j) * kBxBytes, kBxBytes, &h_full[s]);
           ++t;
         }
       }
@@ -1072,6 +1084,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
           if (!live(a, b, tm, j)) continue;
           const int s = t % ST, as = t % NSB;
           TMC_PROF_WAIT_M(3, mbar_wait(&t_full[s], (t / ST) & 1));
+          mbar_wait(&h_full[s], (t / ST) & 1);
           TMC_PROF_WAIT_M(4, mbar_wait(&s_empty[as], ((t / NSB) & 1) ^ 1));
           TMC_PROF_WAIT_M(17, tc_fence_after());
           const uint32_t d = tmem + (uint32_t)(as * 128);
@@ -1094,9 +1107,12 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
               mma_f16(d, dadd(dO, o), dadd(dS, o), IDESC_S, 1u);
             }
           }
+          // + the streamed term ht (log2 units) on the tensor core: ones(128 x 16) . [parts hi/lo]^T
+          if (!(a.dbg & 1)) mma_f16(d, sdesc_bx(smem_u32(sOnes)), sdesc_bx(smem_u32(sHx) + s * kBxBytes), IDESC_S, 1u);
           TMC_PROF_END_M(15, _ts);
           TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
+          mma_commit(&h_empty[s]);
           TMC_PROF_END_M(18, _tc2);
           if (!TMC_BWD_SPLIT && jj > 0) grad(a, t - 1, jj == 1);
           ++jj;
@@ -1137,14 +1153,12 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
 #endif
     // P~ of 32 columns: arguments S + ht + (ho + 14) on packed pairs, ex2, row-sum accumulation,
     // fp16 hi/lo split
-    auto chunk_math = [&](const uint32_t* v, const float4* hts, float2 hom2, float2* racc, uint32_t* hi, uint32_t* lo) {
+    auto chunk_math = [&](const uint32_t* v, float2 hom2, float2* racc, uint32_t* hi, uint32_t* lo) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 h4 = hts[q];
-        const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
-                                                 make_float2(h4.x, h4.y)), hom2);
-        const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
-                                                 make_float2(h4.z, h4.w)), hom2);
+        // S already carries the streamed term (bias MMA); + the owned term (ho + 14)
+        const float2 y01 = __fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])), hom2);
+        const float2 y23 = __fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])), hom2);
         const bool poly = q >= 8 - TMC_BWD_NPOLY;
         const float2 p01 = poly ? make_float2(ex2_poly(y01.x), ex2_poly(y01.y)) : make_float2(ex2(y01.x), ex2(y01.y));
         const float2 p23 = poly ? make_float2(ex2_poly(y23.x), ex2_poly(y23.y)) : make_float2(ex2(y23.x), ex2(y23.y));
@@ -1178,7 +1192,6 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         const int as = t % NSB, s = t % ST;
         TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
-        TMC_PROF_WAIT(sw == 0 && lane == 0, 9, mbar_wait(&h_full[s], (t / ST) & 1));
         TMC_SMX_MARK(0);
         if constexpr (SG == 3) {
           // two column quarters, both TMEM loads in flight before the first wait
@@ -1190,12 +1203,11 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
           tmem_ld_wait();
           TMC_SMX_MARK(1);
           uint32_t hi[16], lo[16];
-          const float4* hts0 = reinterpret_cast<const float4*>(sHt + s * 128 + cq0 * 32);
-          if (hom > -INFINITY) chunk_math(v0, hts0, hom2, racc, hi, lo);
+          if (hom > -INFINITY) chunk_math(v0, hom2, racc, hi, lo);
           else for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
           TMC_ST16(ta0, hi);
           if constexpr (PLO) TMC_ST16(ta0 + 16, lo);
-          if (hom > -INFINITY) chunk_math(v1, hts0 + 8, hom2, racc, hi, lo);
+          if (hom > -INFINITY) chunk_math(v1, hom2, racc, hi, lo);
           TMC_SMX_MARK(2);
           TMC_ST16(ta1, hi);
           if constexpr (PLO) TMC_ST16(ta1 + 16, lo);
@@ -1214,35 +1226,9 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
 #pragma unroll
             for (int q = 0; q < 32; ++q) v[q] = 0u;
           }
-          const float4* hts = reinterpret_cast<const float4*>(sHt + s * 128 + cq * 32);
           uint32_t hi[16], lo[16];
           if (hom > -INFINITY && !(a.dbg & 4)) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 h4 = hts[q];
-              // arguments on packed pairs: S + ht + (ho + 14)
-              const float2 y01 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1])),
-                                                       make_float2(h4.x, h4.y)), hom2);
-              const float2 y23 = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])),
-                                                       make_float2(h4.z, h4.w)), hom2);
-              // the last TMC_BWD_NPOLY of the 8 groups of 4 exponentials run on the FMA pipe
-              const bool poly = q >= 8 - TMC_BWD_NPOLY;
-              const float2 p01 = poly ? make_float2(ex2_poly(y01.x), ex2_poly(y01.y)) : make_float2(ex2(y01.x), ex2(y01.y));
-              const float2 p23 = poly ? make_float2(ex2_poly(y23.x), ex2_poly(y23.y)) : make_float2(ex2(y23.x), ex2(y23.y));
-              racc[0] = __fadd2_rn(racc[0], p01);
-              racc[1] = __fadd2_rn(racc[1], p23);
-              __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
-              hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
-              hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
-              if constexpr (PLO) {
-                const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-                const float2 d01 = __fadd2_rn(p01, make_float2(-f01.x, -f01.y));
-                const float2 d23 = __fadd2_rn(p23, make_float2(-f23.x, -f23.y));
-                __half2 l01 = __floats2half2_rn(d01.x, d01.y), l23 = __floats2half2_rn(d23.x, d23.y);
-                lo[2 * q] = *reinterpret_cast<uint32_t*>(&l01);
-                lo[2 * q + 1] = *reinterpret_cast<uint32_t*>(&l23);
-              }
-            }
+            chunk_math(v, hom2, racc, hi, lo);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
@@ -1254,7 +1240,6 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&h_empty[s]);
         if (!(a.dbg & 16)) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -1410,6 +1395,7 @@ struct RowtermArgs {
   const float *ell, *w, *beta;   // [B][R], [B][R], [B][betaStride] (UP: beta of the row side) or NULL
   int betaStride, R, Rpad;
   float* rterm2;                 // [B][Rpad]
+  uint8_t* bx;                   // [B][Rpad/128][kBxBytes]: rterm2 as the bias operand of the column-owner pass
   float* sgn;                    // [B]
   int* live;                     // [B][Rpad/128] 1 if any row of the 128-row tile carries weight
 };
@@ -1447,6 +1433,7 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
       }
     }
     a.rterm2[(size_t)b * a.Rpad + r] = v;
+    if (a.bx) store_bias_row(a.bx + (size_t)b * (a.Rpad / kTileRows) * kBxBytes, r, v);
     if (v > -INFINITY) s_live[r / kTileRows] = 1;
   }
   __syncthreads();
@@ -1477,7 +1464,7 @@ constexpr int kDefaultBwdGroups = 3;   // 8 softmax warps, two column quarters e
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
-  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, sgn = 0, rlive = 0, clive = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, rbx = 0, sgn = 0, rlive = 0, clive = 0;
   bool bwd_ok = false;      // reverse pass on tensor cores
 };
 
@@ -1521,6 +1508,7 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     t.bx = tc_carve(cur, Bn * (Cpad / 128) * tc::kBxBytes);
     t.shift = tc_carve(cur, Bn * D[i] * 4);
     t.rterm2 = tc_carve(cur, Bn * Rpad * 4);
+    t.rbx = tc_carve(cur, Bn * (Rpad / 128) * tc::kBxBytes);
     t.rlive = tc_carve(cur, Bn * (Rpad / 128) * 4);
     t.clive = tc_carve(cur, Bn * (Cpad / 128) * 4);
     t.sgn = tc_carve(cur, Bn * 4);
@@ -1727,6 +1715,7 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
         r.beta = zrows ? nullptr : reinterpret_cast<const float*>(w + t.beta);
         r.betaStride = t.KpPad; r.R = a.R; r.Rpad = Rpad;
         r.rterm2 = rterm2; r.sgn = sgn;
+        r.bx = w + t.rbx;
         r.live = reinterpret_cast<int*>(w + t.rlive);
       }
       tc::BwdArgs& f = fb.e[k];
@@ -1739,6 +1728,9 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
       f.t_tiles = (own_rows ? Cpad : Rpad) / 128;
       f.ho = own_rows ? rterm2 : reinterpret_cast<const float*>(w + t.cb2);
       f.ht = own_rows ? reinterpret_cast<const float*>(w + t.cb2) : rterm2;
+      // the same streamed term as bias-operand tiles: the forward's column-bias tiles (row-owner
+      // pass) or the row-term tiles written by tc_rowterm_kernel (column-owner pass)
+      f.Hx = own_rows ? w + t.bx : w + t.rbx;
       f.sgn = sgn;
       f.M = own_rows ? a.R : a.C;
       f.B = a.B;
