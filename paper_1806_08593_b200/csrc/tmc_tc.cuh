@@ -1189,7 +1189,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
       for (int j = 0; j < a.t_tiles; ++j) {
         if (!live(a, b, tm, j)) continue;
         if (SG == 2 && (int)(t & 1) != grp) { ++t; continue; }
-        const int as = t % NSB, s = t % ST;
+        const int as = t % NSB;
         TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
         TMC_SMX_MARK(0);
