@@ -1571,12 +1571,13 @@ inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in,
 }
 
 // Forward softmax variant (TMC_FWD_VARIANT overrides):
-//   0 = tile max + lazy rescale, 1 = optimistic reference (no per-tile max), 2 = 1 + 2/16 polynomial exps.
-constexpr int kDefaultFwdVariant = 0;
+//   0 = tile max + lazy rescale, 1 = optimistic reference (no per-tile max; wrong on wide dynamic
+//   ranges, experiment only), 2 = 1 + 2/16 polynomial exps, 3/4/5 = 0 + 2/16, 3/16, 4/16 polynomial exps.
+constexpr int kDefaultFwdVariant = 4;   // tile max + 3 of every 16 exponentials on the FMA pipe
 inline int tc_fwd_variant() {
   const char* e = std::getenv("TMC_FWD_VARIANT");
   const int v = e ? std::atoi(e) : kDefaultFwdVariant;
-  return (v >= 0 && v <= 2) ? v : kDefaultFwdVariant;
+  return (v >= 0 && v <= 5) ? v : kDefaultFwdVariant;
 }
 
 template <int D, int NPOLY, bool MF>
@@ -1595,6 +1596,9 @@ inline void tc_fwd_launch(const tc::FwdBatch& fb, cudaStream_t s) {
   switch (tc_fwd_variant()) {
     case 1: return tc_fwd_launch_t<D, 0, true>(fb, s);
     case 2: return tc_fwd_launch_t<D, 2, true>(fb, s);
+    case 3: return tc_fwd_launch_t<D, 2, false>(fb, s);
+    case 4: return tc_fwd_launch_t<D, 3, false>(fb, s);
+    case 5: return tc_fwd_launch_t<D, 4, false>(fb, s);
     default: return tc_fwd_launch_t<D, 0, false>(fb, s);
   }
 }
