@@ -20,11 +20,15 @@ grads = tmc.alloc_grads(g)
 s = torch.cuda.current_stream()
 pairs = B * sum(wl.K[i] * wl.Kp(i) for i in range(len(wl.parent)) if wl.parent[i] >= 0)
 for st in settings:
-    parts = st.split(":") + ["0"] * 3
-    flags, gt, poly = parts[0], parts[1] or "3", parts[2] or "0"
+    parts = st.split(":") + [""] * 3
+    flags, gt, poly = parts[0] or "0", parts[1] or "3", parts[2]
     os.environ["TMC_DEBUG_FLAGS"] = flags
     os.environ["TMC_BWD_GRAD_TERMS"] = gt
-    os.environ["TMC_FWD_VARIANT"] = poly
+    if poly:
+        os.environ["TMC_FWD_VARIANT"] = poly
+    else:                                   # the library default
+        os.environ.pop("TMC_FWD_VARIANT", None)
+        poly = "-1"
     for _ in range(2):
         tmc.tmc_forward(g, inp, logp, ws, None, s); tmc.tmc_backward(g, inp, ws, None, grads, None, None, s)
     torch.cuda.synchronize()
