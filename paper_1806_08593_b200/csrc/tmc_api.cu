@@ -375,7 +375,7 @@ void launch_pad(const std::vector<simt::PadDesc>& jobs, int unpad, cudaStream_t 
     int64_t mx = 1;
     for (int k = 0; k < pb.count; ++k) {
       pb.d[k] = jobs[j0 + k];
-      mx = std::max<int64_t>(mx, pb.d[k].rows * (unpad ? pb.d[k].Di : pb.d[k].Dt));
+      mx = std::max<int64_t>(mx, pb.d[k].rows * (unpad ? pb.d[k].Di : pb.d[k].Dt / 4));
     }
     const unsigned gx = (unsigned)std::min<int64_t>((mx + 255) / 256, 1024);
     simt::pad_batch_kernel<<<dim3(gx, pb.count), 256, 0, s>>>(pb, unpad);

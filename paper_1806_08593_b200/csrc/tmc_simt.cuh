@@ -451,13 +451,28 @@ struct PadDesc { const float* src; float* dst; int64_t rows; int Di, Dt; float f
 struct PadBatch { PadDesc d[kMaxPad]; int count; };
 __global__ void __launch_bounds__(256) pad_batch_kernel(const __grid_constant__ PadBatch pb, int unpad) {
   const PadDesc& q = pb.d[blockIdx.y];
-  const int W = unpad ? q.Di : q.Dt;
-  const int64_t n = q.rows * W;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t / W;
-    const int d = (int)(t - r * W);
-    if (unpad) q.dst[t] = q.src[r * q.Dt + d];
-    else q.dst[t] = d < q.Di ? q.src[r * q.Di + d] : q.fill;
+  if (unpad) {
+    const int64_t n = q.rows * q.Di;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = t / q.Di;
+      q.dst[t] = q.src[r * q.Dt + (t - r * q.Di)];
+    }
+    return;
+  }
+  // padded rows of Dt = 32 / 64 floats written as float4 (Dt / 4 = 8 or 16 per row: shift, no divide)
+  const int sh = q.Dt == 64 ? 4 : 3;
+  const int64_t n4 = q.rows << sh;
+  float4* dst4 = reinterpret_cast<float4*>(q.dst);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t >> sh;
+    const int d0 = (int)(t - (r << sh)) * 4;
+    const float* sr = q.src + r * q.Di;
+    float4 v;
+    v.x = d0 < q.Di ? sr[d0] : q.fill;
+    v.y = d0 + 1 < q.Di ? sr[d0 + 1] : q.fill;
+    v.z = d0 + 2 < q.Di ? sr[d0 + 2] : q.fill;
+    v.w = d0 + 3 < q.Di ? sr[d0 + 3] : q.fill;
+    dst4[t] = v;
   }
 }
 __global__ void __launch_bounds__(256) pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,

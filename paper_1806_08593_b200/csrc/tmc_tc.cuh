@@ -427,7 +427,10 @@ struct ColbiasArgs {
   double* off_out;
 };
 
-struct ColbiasBatch { ColbiasArgs e[16]; int ne; };
+// Edges per batched launch (forward, reverse, column bias, row terms): the siblings of one tree
+// level share a persistent grid.  Kernel parameters up to 32 KB (CUDA >= 12.1) hold the batch.
+constexpr int kMaxBatch = 32;
+struct ColbiasBatch { ColbiasArgs e[kMaxBatch]; int ne; };
 
 // Row r of a K=16 bias operand tile (the extra MMA that adds a per-column term to S): the value as
 // four fp16-representable parts (each within +-60000 log2 units), every part as fp16 hi + lo in
@@ -514,7 +517,7 @@ struct FwdArgs {
 
 // Several independent edges (siblings of a tree level) in one persistent launch: unit u belongs to
 // edge e with ustart[e] <= u < ustart[e+1].  All edges of a batch share D.
-constexpr int kMaxBatch = 16;
+// (kMaxBatch is defined with the colbias batch above)
 struct FwdBatch {
   FwdArgs e[kMaxBatch];
   int ustart[kMaxBatch + 1];
@@ -1400,7 +1403,7 @@ struct RowtermArgs {
   int* live;                     // [B][Rpad/128] 1 if any row of the 128-row tile carries weight
 };
 
-struct RowtermBatch { RowtermArgs e[16]; int ne; };
+struct RowtermBatch { RowtermArgs e[kMaxBatch]; int ne; };
 
 __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__ RowtermBatch rb_) {
   const RowtermArgs& a = rb_.e[blockIdx.y];
