@@ -456,7 +456,13 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
     }
     L.K = p.K[i]; L.Kp = p.Kp[i]; L.D = p.D[i]; L.parent = p.parent[i];
   }
-  return small::smem_bytes(*A) <= 160 * 1024;
+  A->cache = 0;
+  if (small::smem_bytes(*A) > 160 * 1024) return false;
+  if (mode == 1) {                            // keep the forward's factor tiles for the reverse sweep if they fit
+    A->cache = 1;
+    if (small::smem_bytes(*A) > 160 * 1024) A->cache = 0;
+  }
+  return true;
 }
 
 tmc_status launch_small(const small::Args& A, cudaStream_t s) {

@@ -22,6 +22,7 @@ struct Lat {
 struct Args {
   Lat l[kMaxN];
   int n, B, mode;                              // mode 0: logp only; 1: logp + gradients
+  int cache;                                   // 1: keep every latent's factor tile from the forward sweep (mode 1)
   float alpha;
   const double* dlogp;
   double* logp;
@@ -41,6 +42,8 @@ __host__ inline size_t smem_bytes(const Args& a) {
     kp = L.Kp > kp ? L.Kp : kp;
   }
   f += (size_t)kk * kp;
+  if (a.cache)
+    for (int i = 0; i < a.n; ++i) f += r4((size_t)a.l[i].K * a.l[i].Kp);   // per-latent factor tiles
   return 8 * d + 4 * f + 64;
 }
 
@@ -82,6 +85,9 @@ __device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
   }
 }
 
+__device__ __forceinline__ int kkmax(const Args& a) { int m = 1; for (int i = 0; i < a.n; ++i) m = a.l[i].K > m ? a.l[i].K : m; return m; }
+__device__ __forceinline__ int kpmax(const Args& a) { int m = 1; for (int i = 0; i < a.n; ++i) m = a.l[i].Kp > m ? a.l[i].Kp : m; return m; }
+
 __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -105,6 +111,14 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
     ST[i].ldet = fp; fp += r4(L.Kp);
   }
   float* F = fp;
+  float* FC[kMaxN];                           // per-latent factor tiles (cache) or the shared scratch
+  {
+    float* q = fp + r4(kkmax(A) * kpmax(A));
+    for (int i = 0; i < A.n; ++i) {
+      if (A.cache) { FC[i] = q; q += r4(A.l[i].K * A.l[i].Kp); }
+      else FC[i] = F;
+    }
+  }
   // stage this datapoint's inputs once (all copies in flight together); later phases read shared memory
   for (int i = 0; i < A.n; ++i) {
     const Lat& L = A.l[i];
@@ -146,14 +160,15 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   double logp = 0.0;
   for (int i = A.n - 1; i >= 0; --i) {          // parent[i] < i: children come first
     const Lat& L = A.l[i];
-    factor(L, ST[i], A.alpha, F);
+    float* Fi = FC[i];
+    factor(L, ST[i], A.alpha, Fi);
     __syncthreads();
     // one warp per column c, lanes over a (K <= 64): warp-shuffle max and sum
     const int warp = tid >> 5, lane = tid & 31;
     const double lnK = log((double)L.K);
     for (int c = warp; c < L.Kp; c += kThreads / 32) {
-      const double x0 = lane < L.K ? (double)F[lane * L.Kp + c] + H[i][lane] : -INFINITY;
-      const double x1 = lane + 32 < L.K ? (double)F[(lane + 32) * L.Kp + c] + H[i][lane + 32] : -INFINITY;
+      const double x0 = lane < L.K ? (double)Fi[lane * L.Kp + c] + H[i][lane] : -INFINITY;
+      const double x1 = lane + 32 < L.K ? (double)Fi[(lane + 32) * L.Kp + c] + H[i][lane + 32] : -INFINITY;
       double m = fmax(x0, x1);
 #pragma unroll
       for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -178,7 +193,8 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   const double w = (logp == -INFINITY) ? 0.0 : (A.dlogp ? A.dlogp[b] : 1.0);
   for (int i = 0; i < A.n; ++i) {
     const Lat& L = A.l[i];
-    factor(L, ST[i], A.alpha, F);
+    float* F = FC[i];                        // the forward sweep's factor tile when cached
+    if (!A.cache) factor(L, ST[i], A.alpha, F);
     __syncthreads();
     // P (in place of F): weight of pair (a, c)
     for (int t = tid; t < L.K * L.Kp; t += kThreads) {
