@@ -5,18 +5,22 @@
 //   log N(z_a; mu_c, diag e^{v_c}) = S[a,c] + beta[c],   S = X . Y^T,
 //   X[a] = [z'^2, z'],  Y[c] = [-lam/2, lam mu'] * log2(e),  lam = e^{-v},
 //   beta[c] = -1/2 sum_d (lam mu'^2 + v + ln 2 pi),  z' = z - s,  mu' = mu - s
-// with a per-(datapoint, latent) centering shift s = mean_c mu (an exact identity that keeps the
-// expanded terms small).  Every operand is split into an fp16 pair (hi, lo = fp16(x - hi)) and
+// with a per-(datapoint, latent) centering shift s (the posterior-weighted mean of the samples the
+// message pass already weighted; an exact identity that keeps the expanded terms small).  Every operand is split into an fp16 pair (hi, lo = fp16(x - hi)) and
 // S = X_hi Y_hi + X_hi Y_lo + X_lo Y_hi is accumulated in fp32 in TMEM by tcgen05.mma kind::f16
 // (relative error ~2^-21 per product).
 //
 //   tc_prep_kernel   (K1): per (datapoint, latent): s, X/Y hi/lo tile images (pre-swizzled 128B,
 //                          the exact shared-memory image a bulk copy lands), beta.
 //   tc_colbias_kernel:     per (datapoint, edge): cbmax, fp64 offset, column bias in log2 units.
-//   tc_fwd_kernel    (K3): persistent, warp-specialised: warp 0 streams tiles with cp.async.bulk
-//                          (TMA engine) into a 3-stage mbarrier ring, warp 1 issues tcgen05.mma
-//                          into double-buffered TMEM accumulators, 4*RB softmax warps drain TMEM
-//                          with tcgen05.ld and run the online-max log2-sum-exp2 (ex2.approx, MUFU).
+//   tc_fwd_kernel    (K3): persistent, warp-specialised: a producer warp streams tiles with
+//                          cp.async.bulk (TMA engine) into a 3-stage mbarrier ring, an MMA warp
+//                          issues tcgen05.mma (+ one K=16 bias MMA) into double-buffered TMEM
+//                          accumulators, 8*RB softmax warps drain TMEM with tcgen05.ld and run the
+//                          online-max log2-sum-exp2 (ex2.approx on MUFU, 3/16 on an FMA polynomial).
+//   tc_rowterm_kernel:     per (datapoint, edge): reverse-pass row terms, their bias tiles, live flags.
+//   tc_bwd_kernel    (K4): one owner pass of the reverse contraction (below).
+//   tc_factors_kernel(K2): materialised logf (tmc_factors).
 #pragma once
 #include <algorithm>
 #include <cstddef>
@@ -780,13 +784,15 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
 //   P~[m,n] = ex2(S2[m,n] + ho[m] + ht[n] + 14)          (= 2^14 |w|/wscale exp(logf + bias - ell))
 //   G[m,:] += sum_n P~[m,n] T[n,:]                         (tcgen05, P~ and T both fp16 hi/lo)
 //   rowsum[m] = sum_n P~[m,n]
-// S is recomputed on tensor cores exactly as in the forward.  P~ is split into fp16 hi/lo and
-// stored back into the TMEM columns its S tile came from (hi in the first 32 columns of each
-// 64-column half, lo in the second), where it is the A operand (tcgen05.mma A-from-TMEM) of the
-// gradient GEMM whose B operand is the streamed tile itself read MN-major; the S buffer is released
-// to the next S MMA by the commit of that gradient GEMM.  Eight softmax warps: two per TMEM lane
-// quarter, each owning one 64-column half of the tile.  The epilogue turns G into dz (T = Y tiles)
-// or dmu/dlogvar (T = X tiles).
+// S is recomputed on tensor cores exactly as in the forward, and the streamed term ht is added by
+// the tensor core too (a K=16 bias MMA on pre-split tiles), so the softmax computes
+// ex2(S + ho + 14) with one FADD2 per pair.  P~ is split into fp16 hi/lo and stored back into the
+// TMEM columns its S tile came from (hi in the first 16 of each 32-column quarter, lo in the last
+// 16), where it is the A operand (tcgen05.mma A-from-TMEM) of the gradient GEMM whose B operand is
+// the streamed tile itself read MN-major; the S buffer is released to the next S MMA by the commit
+// of that gradient GEMM.  Two MMA-issuing warps (S MMAs / gradient GEMMs), eight softmax warps (SG =
+// 3: TMEM lane quarter x column half, two 32-column quarters each), four epilogue warps that turn G
+// into dz (T = Y tiles) or dmu/dlogvar (T = X tiles).
 struct BwdArgs {
   const uint8_t *Ot, *Tt;      // owned / streamed tile images [B][tiles][TILE]
   int o_tiles, t_tiles;
