@@ -85,7 +85,11 @@ typedef enum {
                      /* pads only when K_i, K_p >= 128                                       */
 } tmc_precision;
 
-enum { TMC_FLAG_VALIDATE = 1u };
+enum {
+  TMC_FLAG_VALIDATE = 1u,      /* scan every input for NaN/+inf first (TMC_ERR_NONFINITE), synchronous   */
+  TMC_FLAG_DENSE_REVERSE = 2u  /* reverse pass computes every tile, including tiles whose pair weights   */
+                               /* are all exactly 0 (skipped by default; identical results, measurement) */
+};
 
 typedef struct {
   int32_t n;              /* number of latent variables, >= 1                                 */
@@ -229,6 +233,22 @@ int32_t tmc_version(void);
 
 /* Diagnostics: number of kernels libtmc has launched in this process so far (all streams). */
 uint64_t tmc_launch_count(void);
+
+/* Diagnostics: per-kernel-family device time (bench.py's roofline).  tmc_profile_begin
+ * synchronises the device, clears the counters and enables recording: until tmc_profile_end,
+ * every libtmc launch is bracketed by a CUDA event pair recorded on its launching stream, and the
+ * tensor-core kernels add the tcgen05 MMA flops they issue (live tiles only) to a device counter.
+ * tmc_profile_end synchronises, disables recording and writes one entry per family that launched
+ * (at most max_entries) to HOST `out`; it returns the number of entries or a negative tmc_status.
+ * Not thread-safe against concurrent begin/end; not for use during CUDA-graph capture. */
+typedef struct {
+  const char *family;   /* static string: kernel family name                                */
+  uint64_t launches;    /* launches recorded                                                */
+  double ms;            /* summed device time between each launch's event pair              */
+  double mma_flops;     /* tcgen05 flops the family issued (0 for non-tensor-core families) */
+} tmc_profile_entry;
+int32_t tmc_profile_begin(void);
+int32_t tmc_profile_end(tmc_profile_entry *out, int32_t max_entries);
 
 #ifdef __cplusplus
 }

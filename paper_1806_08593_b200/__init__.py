@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("TMC_LIB_PATH") or os.path.join(_HERE, "libtmc.so")
 TMC_DIR_AUTO, TMC_DIR_DOWN, TMC_DIR_UP = 0, 1, 2
 TMC_PREC_AUTO, TMC_PREC_SIMT, TMC_PREC_TC = 0, 1, 2
 TMC_FLAG_VALIDATE = 1
+TMC_FLAG_DENSE_REVERSE = 2
 
 STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_ERR_GRAPH",
           -4: "TMC_ERR_ALIGNMENT", -5: "TMC_ERR_WORKSPACE", -6: "TMC_ERR_UNSUPPORTED_DEVICE",
@@ -27,7 +28,7 @@ EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "
            "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal",
            "tmc_iwae_workspace_size", "tmc_iwae",
            "tmc_estimate_host_workspace_size", "tmc_estimate_host",
-           "tmc_last_error", "tmc_version", "tmc_launch_count"]
+           "tmc_last_error", "tmc_version", "tmc_launch_count", "tmc_profile_begin", "tmc_profile_end"]
 
 
 class TmcError(RuntimeError):
@@ -45,6 +46,11 @@ class tmc_graph(ctypes.Structure):
 
 class tmc_latent_in(ctypes.Structure):
     _fields_ = [(k, ctypes.c_void_p) for k in ("z", "mu", "logvar", "logq", "logobs")]
+
+
+class tmc_profile_entry(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_char_p), ("launches", ctypes.c_uint64), ("ms", ctypes.c_double),
+                ("mma_flops", ctypes.c_double)]
 
 
 class tmc_latent_grad(ctypes.Structure):
@@ -89,6 +95,10 @@ def load_library(path: str = LIB_PATH):
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
         lib.tmc_launch_count.restype = ctypes.c_uint64
+        lib.tmc_profile_begin.restype = ctypes.c_int32
+        lib.tmc_profile_begin.argtypes = []
+        lib.tmc_profile_end.restype = ctypes.c_int32
+        lib.tmc_profile_end.argtypes = [ctypes.POINTER(tmc_profile_entry), ctypes.c_int32]
         _lib = lib
     return _lib
 
@@ -270,6 +280,21 @@ def tmc_version() -> int:
 
 def tmc_launch_count() -> int:
     return load_library().tmc_launch_count()
+
+
+def tmc_profile_begin() -> None:
+    """Start recording per-kernel-family device time and issued tensor-core flops (diagnostics)."""
+    _check(load_library().tmc_profile_begin())
+
+
+def tmc_profile_end() -> Dict[str, Dict]:
+    """Stop recording; {family: {"launches", "ms", "mma_flops"}} since tmc_profile_begin."""
+    arr = (tmc_profile_entry * 16)()
+    n = load_library().tmc_profile_end(arr, 16)
+    if n < 0:
+        _check(n)
+    return {arr[i].family.decode(): {"launches": int(arr[i].launches), "ms": float(arr[i].ms),
+                                     "mma_flops": float(arr[i].mma_flops)} for i in range(n)}
 
 
 # ----------------------------------------------------------------------------- convenience

@@ -44,6 +44,7 @@ struct Plan {
   int requested_dir = 0;           // the caller's tmc_direction (dir is the resolved one)
   float alpha = 1.f;
   bool dense = false;
+  bool dense_reverse = false;      // TMC_FLAG_DENSE_REVERSE: no zero-weight tile skipping
   std::vector<int> parent, K, D, Kp;
   std::vector<std::vector<int>> children;
   std::vector<int> roots;
@@ -86,6 +87,7 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
     return fail(TMC_ERR_INVALID_ARG, "factor_power must be in [0, 64] (0 = 1)");
   p.alpha = g->factor_power == 0.f ? 1.f : g->factor_power;
   p.dense = dense;
+  p.dense_reverse = (g->flags & TMC_FLAG_DENSE_REVERSE) != 0;
   p.parent.assign(g->parent, g->parent + g->n);
   p.K.assign(g->K, g->K + g->n);
   p.D.assign(g->D, g->D + g->n);
@@ -206,6 +208,7 @@ void launch_pass_t(const PassArgs& a, cudaStream_t s) {
   static bool attr[kMaxDevices] = {};
   ensure_smem_attr(kern, 200 * 1024, attr);
   dim3 grid((NO + simt::kOPC - 1) / simt::kOPC, a.B);
+  ProfScope ps(PF_SIMT, s);
   kern<<<grid, simt::kThreads, smem, s>>>(a);
     TMC_COUNT_LAUNCH();
 }
@@ -225,6 +228,7 @@ void launch_pass(const PassArgs& a, bool zrows, int mode, bool dense, cudaStream
   if (a.B == 0) return;
   if (zrows && !dense && a.C == 1) {   // root of a DOWN chain: K x 1 pair matrix (prior)
     const unsigned grid = (unsigned)(((int64_t)a.B * a.R + 255) / 256);
+    ProfScope ps(PF_SIMT, s);
     if (mode == 0) simt::root_down_fwd_kernel<<<grid, 256, 0, s>>>(a);
     else if (mode == 1) simt::root_down_row_kernel<<<grid, 256, 0, s>>>(a);
     else simt::root_down_col_kernel<<<a.B, 256, 0, s>>>(a);
@@ -257,6 +261,7 @@ void launch_pass_batch_t(const PassArgs* as, int ne, cudaStream_t s) {
       maxD = std::max(maxD, pb.e[k].D);
     }
     dim3 grid((maxNO + simt::kOPC - 1) / simt::kOPC, as[0].B, n);
+    ProfScope ps(PF_SIMT, s);
     kern<<<grid, simt::kThreads, simt::pass_smem_bytes(maxD, DENSE), s>>>(pb);
     TMC_COUNT_LAUNCH();
   }
@@ -378,6 +383,7 @@ void launch_pad(const std::vector<simt::PadDesc>& jobs, int unpad, cudaStream_t 
       mx = std::max<int64_t>(mx, pb.d[k].rows * (unpad ? pb.d[k].Di : pb.d[k].Dt / 4));
     }
     const unsigned gx = (unsigned)std::min<int64_t>((mx + 255) / 256, 1024);
+    ProfScope ps(PF_AUX, s);
     simt::pad_batch_kernel<<<dim3(gx, pb.count), 256, 0, s>>>(pb, unpad);
     TMC_COUNT_LAUNCH();
   }
@@ -440,8 +446,6 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
               double* logp, const double* dlogp, int mode) {
   if (dense || p.requested_prec != TMC_PREC_AUTO || p.requested_dir != TMC_DIR_AUTO || p.n > small::kMaxN)
     return false;
-  static const bool off = std::getenv("TMC_NO_SMALL") != nullptr;
-  if (off) return false;
   for (int i = 0; i < p.n; ++i)
     if (p.K[i] > small::kMaxK || p.Kp[i] > small::kMaxK || p.D[i] > small::kMaxD) return false;
   if (!A) return true;
@@ -469,6 +473,7 @@ tmc_status launch_small(const small::Args& A, cudaStream_t s) {
   const size_t smem = small::smem_bytes(A);
   static bool attr[kMaxDevices] = {};
   ensure_smem_attr(small::small_kernel, 160 * 1024, attr);
+  ProfScope ps(PF_SMALL, s);
   small::small_kernel<<<A.B, small::kThreads, smem, s>>>(A);
   TMC_COUNT_LAUNCH();
   return launch_check("tmc (small-problem kernel)");
@@ -501,6 +506,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       ub.d[j].uoff = at<double>(ws, p.uoff[i]);
       ub.d[j].K = p.K[i];
     }
+    ProfScope ps(PF_AUX, s);
     simt::unary_prep_kernel<<<dim3(p.B, ub.count), 256, 0, s>>>(ub);
     TMC_COUNT_LAUNCH();
   }
@@ -517,6 +523,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       else launch_pass(a, /*zrows=*/true, 0, dense != nullptr, s);
     }
     const EdgeBuf& last = p.e[p.n - 1];
+    ProfScope ps(PF_AUX, s);
     simt::final_down_fwd_kernel<<<p.B, 256, 0, s>>>(at<float>(ws, last.out), at<double>(ws, last.off),
                                                      p.K[p.n - 1], std::log((float)p.K[p.n - 1]),
                                                      at<float>(ws, p.lse), logp);
@@ -573,6 +580,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
           }
           hb.h = at<float>(ws, p.e[i].h);
           hb.hoff = at<double>(ws, p.e[i].hoff);
+          ProfScope ps(PF_AUX, s);
           simt::hbuild_kernel<<<dim3((p.K[i] + 255) / 256, p.B), 256, 0, s>>>(hb);
           TMC_COUNT_LAUNCH();
           done += hb.nchild;
@@ -617,6 +625,7 @@ tmc_status forward_impl(const Plan& p, const tmc_latent_in* in, const float* con
       rl.out[j] = at<float>(ws, p.e[p.roots[j]].out);
       rl.off[j] = at<double>(ws, p.e[p.roots[j]].off);
     }
+    ProfScope ps(PF_AUX, s);
     simt::final_up_fwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, logp);
     TMC_COUNT_LAUNCH();
   }
@@ -636,8 +645,11 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
   auto grad = [&](int i) -> tmc_latent_grad { return out ? out[i] : tmc_latent_grad{}; };
   if (p.dir == TMC_DIR_DOWN) {
     const int L = p.n - 1;
-    simt::final_down_bwd_kernel<<<dim3((p.K[L] + 255) / 256, p.B), 256, 0, s>>>(
-        at<float>(ws, p.e[L].out), at<float>(ws, p.lse), p.K[L], dlogp, at<float>(ws, p.e[L].w));
+    {
+      ProfScope ps(PF_AUX, s);
+      simt::final_down_bwd_kernel<<<dim3((p.K[L] + 255) / 256, p.B), 256, 0, s>>>(
+          at<float>(ws, p.e[L].out), at<float>(ws, p.lse), p.K[L], dlogp, at<float>(ws, p.e[L].w));
+    }
     TMC_COUNT_LAUNCH();
     for (int i = L; i >= 0; --i) {
       PassArgs a = edge_args(p, i, in, dense, ws);
@@ -647,13 +659,13 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       a.gz = g.dz;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
       const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
-      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 1, s));
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 1, p.dense_reverse, s));
       else launch_pass(a, true, 1, dense != nullptr, s);
       // column owner (param side): colsum -> w of the parent edge; dmu_i, dlogvar_i
       a.gz = nullptr; a.pair = nullptr;
       a.gmu = g.dmu; a.glv = g.dlogvar;
       a.colsum = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].w) : at<float>(ws, p.e[i].colsum);
-      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 2, s));
+      if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 2, p.dense_reverse, s));
       else launch_pass(a, true, 2, dense != nullptr, s);
       pi[i] = at<float>(ws, p.e[i].w);
     }
@@ -662,7 +674,10 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
     rl.B = p.B;
     rl.count = (int)p.roots.size();
     for (int j = 0; j < rl.count; ++j) rl.w[j] = at<float>(ws, p.e[p.roots[j]].w);
-    simt::final_up_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, dlogp);
+    {
+      ProfScope ps(PF_AUX, s);
+      simt::final_up_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(rl, dlogp);
+    }
     TMC_COUNT_LAUNCH();
     // Roots -> leaves by depth: an edge's row-owner pass needs its parent edge's column sums;
     // the edges of one depth are independent and run batched (same D) on tensor cores.
@@ -710,8 +725,8 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
         for (size_t k = 0; k < tcI.size(); ++k)
           if (p.D[tcI[k]] == Dv) { ra.push_back(rowA[k]); ca.push_back(colA[k]); tt.push_back(tcT[k]); }
         if (ra.empty()) continue;
-        g_launches.fetch_add(tc_pass_backward_batch(ra.data(), tt.data(), (int)ra.size(), ws, false, 1, s));
-        g_launches.fetch_add(tc_pass_backward_batch(ca.data(), tt.data(), (int)ca.size(), ws, false, 2, s));
+        g_launches.fetch_add(tc_pass_backward_batch(ra.data(), tt.data(), (int)ra.size(), ws, false, 1, p.dense_reverse, s));
+        g_launches.fetch_add(tc_pass_backward_batch(ca.data(), tt.data(), (int)ca.size(), ws, false, 2, p.dense_reverse, s));
       }
     }
   }
@@ -728,6 +743,7 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       gb.d[j].dlogq = dense ? nullptr : g.dlogq;
       gb.d[j].K = p.K[i];
     }
+    ProfScope ps(PF_AUX, s);
     simt::unary_grad_kernel<<<dim3(std::min<int64_t>(((int64_t)p.B * 64 + 255) / 256, 1024), gb.count), 256, 0, s>>>(gb);
     TMC_COUNT_LAUNCH();
   }
@@ -1126,6 +1142,43 @@ tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double
 }
 
 const char* tmc_last_error(void) { return g_err.c_str(); }
+
+int32_t tmc_profile_begin(void) {
+  Profiler& p = profiler();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(TMC_ERR_CUDA, "tmc_profile_begin: device error");
+  static const unsigned long long zeros[PF_COUNT] = {};
+  if (cudaMemcpyToSymbol(tc::g_tmc_mma_flops, zeros, sizeof(zeros)) != cudaSuccess)
+    return fail(TMC_ERR_CUDA, "tmc_profile_begin: counter reset failed");
+  p.recs.clear();
+  p.used = 0;
+  p.on = true;
+  return TMC_OK;
+}
+
+int32_t tmc_profile_end(tmc_profile_entry* out, int32_t max_entries) {
+  Profiler& p = profiler();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (!p.on) return fail(TMC_ERR_INVALID_ARG, "tmc_profile_end without tmc_profile_begin");
+  p.on = false;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(TMC_ERR_CUDA, "tmc_profile_end: device error");
+  unsigned long long flops[PF_COUNT] = {};
+  cudaMemcpyFromSymbol(flops, tc::g_tmc_mma_flops, sizeof(flops));
+  tmc_profile_entry acc[PF_COUNT];
+  for (int f = 0; f < PF_COUNT; ++f) acc[f] = tmc_profile_entry{prof_name(f), 0, 0.0, (double)flops[f]};
+  for (const Profiler::Rec& r : p.recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+    acc[r.fam].launches += 1;
+    acc[r.fam].ms += ms;
+  }
+  p.recs.clear();
+  p.used = 0;
+  int n = 0;
+  for (int f = 0; f < PF_COUNT && n < max_entries; ++f)
+    if (acc[f].launches) out[n++] = acc[f];
+  return n;
+}
 
 int32_t tmc_version(void) { return 100; }
 

@@ -1,6 +1,8 @@
 // Internal structures shared by the libtmc host code and kernels (NOT part of the ABI).
 #pragma once
 #include <cstdint>
+#include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace tmc {
@@ -27,6 +29,55 @@ inline void ensure_smem_attr(Kernel k, int bytes, bool* done) {
     done[d] = true;
   }
 }
+
+// ------------------------------------------------------------------ launch profiler (diagnostics)
+// tmc_profile_begin/end (include/tmc.h): while enabled, every launch of a kernel family is
+// bracketed by a CUDA event pair recorded on the launching stream, and the tensor-core kernels add
+// the tcgen05 flops they issue to a device counter.  Off by default: a disabled scope is one load.
+enum ProfFamily { PF_TC_FWD = 0, PF_TC_BWD, PF_TC_PREP, PF_SIMT, PF_SMALL, PF_AUX, PF_COUNT };
+inline const char* prof_name(int f) {
+  static const char* n[PF_COUNT] = {"tc_fwd_kernel", "tc_bwd_kernel", "tc_prep (shift/prep/colbias/rowterm)",
+                                    "simt", "small_kernel", "aux (unary/final/pad/iwae/sampler)"};
+  return n[f];
+}
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<cudaEvent_t> pool;   // reused across sessions
+  size_t used = 0;
+  struct Rec { int fam; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+};
+inline Profiler& profiler() {
+  static Profiler p;
+  return p;
+}
+inline bool prof_on() { return profiler().on; }
+struct ProfScope {
+  int fam;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int fam_, cudaStream_t s_) : fam(fam_), s(s_) {
+    Profiler& p = profiler();
+    if (!p.on) return;
+    std::lock_guard<std::mutex> lk(p.mu);
+    while (p.pool.size() < p.used + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      p.pool.push_back(e);
+    }
+    a = p.pool[p.used++];
+    b = p.pool[p.used++];
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    Profiler& p = profiler();
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.recs.push_back({fam, a, b});
+  }
+};
 
 constexpr float kLog2Pi = 1.8378770664093453f;
 constexpr float kLog2E = 1.4426950408889634f;

@@ -38,6 +38,9 @@ namespace tc {
 constexpr int kTileRows = 128;
 constexpr int kAtomBytes = 128 * 128;        // 128 rows x 128 B (one SWIZZLE_128B K-atom)
 
+// tcgen05 flops issued per kernel family while the launch profiler is on (tmc_profile_begin/end)
+__device__ unsigned long long g_tmc_mma_flops[PF_COUNT];
+
 template <int D>
 struct Geo {
   static constexpr int W = 2 * D;                    // fp16 elements per part
@@ -457,12 +460,23 @@ __device__ __forceinline__ void store_bias_row(uint8_t* tiles, int r, float v) {
   *reinterpret_cast<uint4*>(tile + bx_off(rr, 8)) = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// live[t] = 1 if any of the 128 log2 terms of tile t is finite (any number of tiles): one warp per
+// tile, block-stride over tiles, read back from the values this block has just stored.
+__device__ __forceinline__ void tile_live_flags(const float* vals, int ntiles, int* live) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < ntiles; t += nw) {
+    const float* v = vals + (size_t)t * kTileRows;
+    const bool any = (v[lane] > -INFINITY) || (v[lane + 32] > -INFINITY) || (v[lane + 64] > -INFINITY) ||
+                     (v[lane + 96] > -INFINITY);
+    const unsigned m = __ballot_sync(0xffffffffu, any);
+    if (lane == 0) live[t] = m ? 1 : 0;
+  }
+}
+
 __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__ ColbiasBatch cbb_) {
   const ColbiasArgs& a = cbb_.e[blockIdx.y];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[32];
-  __shared__ int s_live[64];
-  if (tid < 64) s_live[tid] = 0;
   const float* cbb = a.cb + (size_t)b * a.C;
   float m = -INFINITY;
   for (int c = tid; c < a.C; c += 256) m = fmaxf(m, cbb[c]);
@@ -486,13 +500,12 @@ __global__ void __launch_bounds__(256) tc_colbias_kernel(const __grid_constant__
       v *= kLog2E;
     }
     a.cb2[(size_t)b * a.Cpad + c] = v;
-    if (v > -INFINITY) s_live[c / kTileRows] = 1;
     if (a.bx) {
       store_bias_row(a.bx + (size_t)b * (a.Cpad / kTileRows) * kBxBytes, c, v);
     }
   }
-  __syncthreads();
-  if (a.live && tid < a.Cpad / kTileRows) a.live[(size_t)b * (a.Cpad / kTileRows) + tid] = s_live[tid];
+  __syncthreads();   // the block's cb2 stores are visible to the whole block
+  if (a.live) tile_live_flags(a.cb2 + (size_t)b * a.Cpad, a.Cpad / kTileRows, a.live + (size_t)b * (a.Cpad / kTileRows));
   if (tid == 0) {
     a.cbmax[b] = cmax;
     double off = (double)cmax;
@@ -516,7 +529,6 @@ struct FwdArgs {
   int R, B;
   float lnC;
   float *out, *ell;            // [B][R]
-  int dbg;                     // experiment flags (TMC_DEBUG_FLAGS; 0 in production): 1 no MMA, 2 no softmax math
 };
 
 // Several independent edges (siblings of a tree level) in one persistent launch: unit u belongs to
@@ -526,6 +538,8 @@ struct FwdBatch {
   FwdArgs e[kMaxBatch];
   int ustart[kMaxBatch + 1];
   int ne;
+  int count;                          // launch profiler on: add issued MMA flops to g_tmc_mma_flops
+  unsigned long long flops_per_tile;  // tcgen05 flops issued per 128 x 128 pair tile
 };
 template <typename Batch>
 __device__ __forceinline__ int batch_edge(const Batch& fb, int u) {
@@ -534,9 +548,13 @@ __device__ __forceinline__ int batch_edge(const Batch& fb, int u) {
   return e;
 }
 
-template <int D, int NPOLY, bool MAXFREE>
+// 3 of every 16 exponentials of the forward run on the FMA pipe (ex2_poly); DESIGN.md §12c.
+constexpr int kFwdPolyExps = 3;
+
+template <int D>
 __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid_constant__ FwdBatch fb) {
   using G = Geo<D>;
+  constexpr int NPOLY = kFwdPolyExps;
   constexpr int RB = G::RB, ST = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared window
@@ -612,6 +630,7 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           bulk_g2s(sB + (size_t)s * G::TILE, a.Bt + ((size_t)b * a.b_tiles + j) * G::TILE, G::TILE, &b_full[s]);
           bulk_g2s(sBx + (size_t)s * kBxBytes, a.Bx + ((size_t)b * a.b_tiles + j) * kBxBytes, kBxBytes, &b_full[s]);
         }
+        if (fb.count) atomicAdd(&g_tmc_mma_flops[PF_TC_FWD], (unsigned long long)a.b_tiles * RB * fb.flops_per_tile);
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
@@ -631,7 +650,6 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           tc_fence_after();
 #pragma unroll
           for (int rb = 0; rb < RB; ++rb) {
-            if (a.dbg & 1) break;
             const uint32_t d = tmem + (uint32_t)((rb * 2 + as) * 128);
             const uint64_t dA = sdesc(aBase + rb * G::TILE), dB = sdesc(bBase + s * G::TILE);
             // small cross terms first, the large hi*hi products last: fewer fp32 accumulator
@@ -689,7 +707,6 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[as]);
-        if (a.dbg & 2) { sum += __uint_as_float(v[0]) + __uint_as_float(v[63]); continue; }
         // x = S + colbias, both from the tensor core (the bias is the extra K=16 MMA)
         float2 x2[32];
 #pragma unroll
@@ -722,30 +739,12 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           const float2 tt = __fadd2_rn(t01, t23);
           return tt.x + tt.y;
         };
-        if constexpr (MAXFREE) {
-          // Optimistic reference: the row's reference mref is the exact max of the first tile with
-          // a finite value and is only raised when a later tile's partial sum leaves the safe range
-          // (overflow / NaN from an argument >= 128): then the tile is redone against its own max.
-          // The first tile contributes ex2(0) = 1, so anything underflowing below it is negligible.
-          if (mref == -INFINITY) mref = tile_max();
-          if (mref > -INFINITY) {
-            float ts = tile_sum(mref);
-            if (!(ts <= 1.0e30f)) {
-              const float tmax = tile_max();
-              sum *= ex2(mref - tmax);
-              mref = tmax;
-              ts = tile_sum(mref);
-            }
-            sum += ts;
-          }
-        } else {
-          const float tmax = tile_max();
-          if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
-            sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
-            mref = tmax;
-          }
-          if (mref > -INFINITY) sum += tile_sum(mref);
+        const float tmax = tile_max();
+        if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
+          sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
+          mref = tmax;
         }
+        if (mref > -INFINITY) sum += tile_sum(mref);
       }
       // merge the two column halves of each row (half 1 -> SMEM -> half 0)
       if (half == 1) sMerge[rloc] = make_float2(mref, sum);
@@ -808,7 +807,6 @@ struct BwdArgs {
   float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
   float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
   const int *olive, *tlive;    // [B][o_tiles], [B][t_tiles]: 0 = every P~ of the tile is exactly 0 (skipped)
-  int dbg;                     // experiment flags: 1 no S MMA, 2 no gradient MMA, 4 no softmax math, 8 half T bytes
 };
 
 template <int D>
@@ -887,6 +885,8 @@ struct BwdBatch {
   BwdArgs e[kMaxBatch];
   int ustart[kMaxBatch + 1];
   int ne;
+  int count;                          // launch profiler on: add issued MMA flops to g_tmc_mma_flops
+  unsigned long long flops_per_tile;  // tcgen05 flops issued per live 128 x 128 pair tile
 };
 
 // SG = softmax groups: 1 = all 16 softmax warps on every tile (one 32-column quarter each);
@@ -1004,21 +1004,21 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         ++ua;
         mbar_expect_tx(o_full, G::TILE);
         bulk_g2s(sO, a.Ot + ((size_t)b * a.o_tiles + mt) * G::TILE, G::TILE, o_full);
+        unsigned long long nlive = 0;
         for (int j = 0; j < a.t_tiles; ++j) {
           if (!tlive(a, b, j)) continue;
+          ++nlive;
           const int s = t % ST;
           const uint32_t ph = ((t / ST) & 1) ^ 1;
           TMC_PROF_WAIT(true, 0, mbar_wait(&t_empty[s], ph));
-          {
-            const uint32_t tb = (a.dbg & 8) ? G::TILE / 2 : G::TILE;   // experiment: half the bytes
-            mbar_expect_tx(&t_full[s], tb);
-            bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, tb, &t_full[s]);
-          }
+          mbar_expect_tx(&t_full[s], G::TILE);
+          bulk_g2s(sT + (size_t)s * G::TILE, a.Tt + ((size_t)b * a.t_tiles + j) * G::TILE, G::TILE, &t_full[s]);
           TMC_PROF_WAIT(true, 1, mbar_wait(&h_empty[s], ph));
           mbar_expect_tx(&h_full[s], kBxBytes);
           bulk_g2s(sHx + (size_t)s * kBxBytes, a.Hx + ((size_t)b * a.t_tiles + j) * kBxBytes, kBxBytes, &h_full[s]);
           ++t;
         }
+        if (fb.count) atomicAdd(&g_tmc_mma_flops[PF_TC_BWD], nlive * fb.flops_per_tile);
       }
     }
     TMC_PROF_END(lane == 0, 14, _tr0);
@@ -1043,7 +1043,6 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         TMC_PROF_T0_M(_tg);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          if (a.dbg & 2) break;
           // P~ of K-step kk: 16 tile columns held by column quarter kk/2, hi then lo (16 TMEM columns each)
           const uint32_t phi = pA + (kk >> 1) * 32 + (kk & 1) * 8, plo = phi + 16;
           const uint64_t thi = dadd(dT, kk * 2048), tlo = dadd(dT, G::PART + kk * 2048);
@@ -1100,7 +1099,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
           const uint64_t dO = sdesc(oBase), dS = sdesc(tBase + s * G::TILE);
           TMC_PROF_T0_M(_ts);
 #pragma unroll
-          for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
+          for (int at = 0; at < G::ATOMS; ++at) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
@@ -1109,7 +1108,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
             }
           }
 #pragma unroll
-          for (int at = 0; at < G::ATOMS && !(a.dbg & 1); ++at) {
+          for (int at = 0; at < G::ATOMS; ++at) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = at * kAtomBytes + kk * 32;
@@ -1117,7 +1116,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
             }
           }
           // + the streamed term ht (log2 units) on the tensor core: ones(128 x 16) . [parts hi/lo]^T
-          if (!(a.dbg & 1)) mma_f16(d, sdesc_bx(smem_u32(sOnes)), sdesc_bx(smem_u32(sHx) + s * kBxBytes), IDESC_S, 1u);
+          mma_f16(d, sdesc_bx(smem_u32(sOnes)), sdesc_bx(smem_u32(sHx) + s * kBxBytes), IDESC_S, 1u);
           TMC_PROF_END_M(15, _ts);
           TMC_PROF_T0_M(_tc2);
           mma_commit(&s_full[as]);
@@ -1227,29 +1226,22 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
           const int cq = (SG == 2) ? (((sw >> 2) & 1) * 2 + c) : (sw >> 2);
           uint32_t v[32];
           const uint32_t taddr = tmem + lane_off + (uint32_t)(as * 128 + cq * 32);
-          if (!(a.dbg & 16)) {     // experiment flag 16: no TMEM traffic from the softmax warps
-            TMC_LD32(taddr, v);
-            tmem_ld_wait();
-            TMC_SMX_MARK(1);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) v[q] = 0u;
-          }
+          TMC_LD32(taddr, v);
+          tmem_ld_wait();
+          TMC_SMX_MARK(1);
           uint32_t hi[16], lo[16];
-          if (hom > -INFINITY && !(a.dbg & 4)) {
+          if (hom > -INFINITY) {
             chunk_math(v, hom2, racc, hi, lo);
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
           }
           TMC_SMX_MARK(2);
-          if (!(a.dbg & 16)) {
-            TMC_ST16(taddr, hi);
-            if constexpr (PLO) TMC_ST16(taddr + 16, lo);
-          }
+          TMC_ST16(taddr, hi);
+          if constexpr (PLO) TMC_ST16(taddr + 16, lo);
         }
         __syncwarp();
-        if (!(a.dbg & 16)) tmem_st_wait();
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
@@ -1416,9 +1408,7 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ float red[8];
   __shared__ int neg;
-  __shared__ int s_live[64];
   if (tid == 0) neg = 0;
-  if (tid < 64) s_live[tid] = 0;
   float wm = 0.f;
   for (int r = tid; r < a.R; r += 256) wm = fmaxf(wm, fabsf(a.w[(size_t)b * a.R + r]));
 #pragma unroll
@@ -1443,32 +1433,20 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
     }
     a.rterm2[(size_t)b * a.Rpad + r] = v;
     if (a.bx) store_bias_row(a.bx + (size_t)b * (a.Rpad / kTileRows) * kBxBytes, r, v);
-    if (v > -INFINITY) s_live[r / kTileRows] = 1;
   }
   __syncthreads();
   if (tid == 0) a.sgn[b] = neg ? -ws : ws;
-  if (tid < a.Rpad / kTileRows) a.live[(size_t)b * (a.Rpad / kTileRows) + tid] = s_live[tid];
+  tile_live_flags(a.rterm2 + (size_t)b * a.Rpad, a.Rpad / kTileRows, a.live + (size_t)b * (a.Rpad / kTileRows));
 }
 
 }  // namespace tc
 
 // ================================================================================ host side
-inline int tc_debug_flags() {   // read per launch (experiments flip it within one process)
-  const char* e = std::getenv("TMC_DEBUG_FLAGS");
-  return e ? std::atoi(e) : 0;
-}
-
-// Zero-weight tile skipping in the reverse pass is exact (the skipped P~ are exactly 0);
-// TMC_DENSE_REVERSE=1 disables it (every tile computed), for measurement.
-inline bool tc_dense_reverse() {
-  const char* e = std::getenv("TMC_DENSE_REVERSE");
-  return e && std::atoi(e) != 0;
-}
-
-// Default number of fp16 terms of the reverse pass's gradient GEMM (TMC_BWD_GRAD_TERMS overrides).
-constexpr int kDefaultGradTerms = 3;
-// Default softmax grouping of the reverse pass (TMC_BWD_SG overrides).
-constexpr int kDefaultBwdGroups = 3;   // 8 softmax warps, two column quarters each (SG = 3)
+// The reverse pass's gradient GEMM uses the 3-term fp16 product (P_lo T_hi + P_hi T_lo + P_hi T_hi,
+// DESIGN.md §6) and 8 wide softmax warps (SG = 3).  Zero-weight tile skipping is exact; the graph
+// flag TMC_FLAG_DENSE_REVERSE disables it (every tile computed, for measurement).
+constexpr int kGradTerms = 3;
+constexpr int kBwdGroups = 3;
 
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
@@ -1565,6 +1543,7 @@ inline int tc_prep_batch(const PrepJob* jobs, int ne, int B, void* ws, cudaStrea
       p.wsrc = j.wsrc; p.wlen = j.wlen; p.wz = j.wz;
       p.alpha = j.alpha;
     }
+    ProfScope ps(PF_TC_PREP, s);
     if (jobs[e0].Di == 32) tc_prep_launch<32>(pb, B, s);
     else tc_prep_launch<64>(pb, B, s);
     launched += 2;   // shift + image kernels
@@ -1579,37 +1558,15 @@ inline int tc_prep_edge(int Ki, int Kpi, int Di, int B, const tmc_latent_in& in,
   return tc_prep_batch(&j, 1, B, ws, s);
 }
 
-// Forward softmax variant (TMC_FWD_VARIANT overrides):
-//   0 = tile max + lazy rescale, 1 = optimistic reference (no per-tile max; wrong on wide dynamic
-//   ranges, experiment only), 2 = 1 + 2/16 polynomial exps, 3/4/5 = 0 + 2/16, 3/16, 4/16 polynomial exps.
-constexpr int kDefaultFwdVariant = 4;   // tile max + 3 of every 16 exponentials on the FMA pipe
-inline int tc_fwd_variant() {
-  const char* e = std::getenv("TMC_FWD_VARIANT");
-  const int v = e ? std::atoi(e) : kDefaultFwdVariant;
-  return (v >= 0 && v <= 5) ? v : kDefaultFwdVariant;
-}
-
-template <int D, int NPOLY, bool MF>
-inline void tc_fwd_launch_t(const tc::FwdBatch& fb, cudaStream_t s) {
+template <int D>
+inline void tc_fwd_launch(const tc::FwdBatch& fb, cudaStream_t s) {
   using G = tc::Geo<D>;
   static bool attr[kMaxDevices] = {};
-  ensure_smem_attr(tc::tc_fwd_kernel<D, NPOLY, MF>, (int)G::SMEM, attr);
+  ensure_smem_attr(tc::tc_fwd_kernel<D>, (int)G::SMEM, attr);
   const int sms = sm_count();
   const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
-  if (grid > 0) tc::tc_fwd_kernel<D, NPOLY, MF><<<grid, G::THREADS, G::SMEM, s>>>(fb);
-}
-
-template <int D>
-inline void tc_fwd_launch(const tc::FwdBatch& fb, cudaStream_t s) {
-  switch (tc_fwd_variant()) {
-    case 1: return tc_fwd_launch_t<D, 0, true>(fb, s);
-    case 2: return tc_fwd_launch_t<D, 2, true>(fb, s);
-    case 3: return tc_fwd_launch_t<D, 2, false>(fb, s);
-    case 4: return tc_fwd_launch_t<D, 3, false>(fb, s);
-    case 5: return tc_fwd_launch_t<D, 4, false>(fb, s);
-    default: return tc_fwd_launch_t<D, 0, false>(fb, s);
-  }
+  if (grid > 0) tc::tc_fwd_kernel<D><<<grid, G::THREADS, G::SMEM, s>>>(fb);
 }
 
 // Forward contraction of ne edges (same D) on tensor cores: per-edge column bias, then ONE persistent
@@ -1651,11 +1608,16 @@ inline int tc_pass_forward_batch(const PassArgs* as, const TcLatentBuf* const* t
       f.out_add = a.rb;
       f.R = a.R; f.B = a.B; f.lnC = a.lnC;
       f.out = a.out; f.ell = a.ell;
-      f.dbg = tc_debug_flags() & 3;
       const int rb = (t.D == 32) ? tc::Geo<32>::RB : tc::Geo<64>::RB;
       fb.ustart[k + 1] = fb.ustart[k] + a.B * (f.a_tiles / rb);
     }
-    tc::tc_colbias_kernel<<<dim3(as[e0].B, cb.ne), 256, 0, s>>>(cb);
+    {
+      ProfScope ps(PF_TC_PREP, s);
+      tc::tc_colbias_kernel<<<dim3(as[e0].B, cb.ne), 256, 0, s>>>(cb);
+    }
+    fb.count = prof_on() ? 1 : 0;
+    fb.flops_per_tile = (unsigned long long)(12 * ts[e0]->D + 32) * 128 * 128;   // 3-term S (K = 2D) + bias MMA (K = 16)
+    ProfScope ps(PF_TC_FWD, s);
     if (ts[e0]->D == 32) tc_fwd_launch<32>(fb, s);
     else tc_fwd_launch<64>(fb, s);
     launched += 2;
@@ -1666,18 +1628,6 @@ inline int tc_pass_forward_batch(const PassArgs* as, const TcLatentBuf* const* t
 inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, cudaStream_t s) {
   const TcLatentBuf* tp = &t;
   return tc_pass_forward_batch(&a, &tp, 1, ws, zrows, s);
-}
-
-inline int tc_grad_terms() {
-  const char* e = std::getenv("TMC_BWD_GRAD_TERMS");
-  const int v = e ? std::atoi(e) : kDefaultGradTerms;
-  return (v >= 1 && v <= 5) ? v : kDefaultGradTerms;
-}
-
-inline int tc_bwd_groups() {
-  const char* e = std::getenv("TMC_BWD_SG");
-  const int v = e ? std::atoi(e) : kDefaultBwdGroups;
-  return (v >= 1 && v <= 3) ? v : kDefaultBwdGroups;
 }
 
 template <int D, int GT, int SG>
@@ -1693,12 +1643,7 @@ inline void tc_bwd_launch_t(const tc::BwdBatch& fb, cudaStream_t s) {
 
 template <int D>
 inline void tc_bwd_launch(const tc::BwdBatch& fb, cudaStream_t s) {
-  const int sg = tc_bwd_groups();
-  switch (tc_grad_terms()) {
-    case 4: return sg == 2 ? tc_bwd_launch_t<D, 4, 2>(fb, s) : tc_bwd_launch_t<D, 4, 1>(fb, s);
-    default: return sg == 2 ? tc_bwd_launch_t<D, 3, 2>(fb, s)
-                   : sg == 3 ? tc_bwd_launch_t<D, 3, 3>(fb, s) : tc_bwd_launch_t<D, 3, 1>(fb, s);
-  }
+  tc_bwd_launch_t<D, kGradTerms, kBwdGroups>(fb, s);
 }
 
 inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.ok && t.bwd_ok && !a.pair; }
@@ -1707,7 +1652,7 @@ inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.o
 // (mode 2), ONE persistent launch over every edge's units.  The row terms are prepared per edge
 // before the row-owner pass.  Returns kernels launched.
 inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* ts, int ne, void* ws, bool zrows,
-                                  int mode, cudaStream_t s) {
+                                  int mode, bool dense_reverse, cudaStream_t s) {
   uint8_t* w = static_cast<uint8_t*>(ws);
   int launched = 0;
   for (int e0 = 0; e0 < ne; e0 += tc::kMaxBatch) {
@@ -1753,23 +1698,25 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
       f.shift = reinterpret_cast<const float*>(w + t.shift);
       f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
       f.rowsum = own_rows ? nullptr : a.colsum;
-      if (!tc_dense_reverse()) {
+      if (!dense_reverse) {
         const int* rl = reinterpret_cast<const int*>(w + t.rlive);
         const int* cl = reinterpret_cast<const int*>(w + t.clive);
         f.olive = own_rows ? rl : cl;
         f.tlive = own_rows ? cl : rl;
       }
-      // experiment flags of the reverse pass: only 2 (no gradient MMA) and 8 (half the streamed
-      // bytes) are honoured; the no-S-MMA / no-softmax-math / no-TMEM variants can deadlock the
-      // pipelined kernel on some shapes and are masked out
-      f.dbg = (tc_debug_flags() >> 2) & (2 | 8);
       f.alpha = a.alpha;
       fb.ustart[k + 1] = fb.ustart[k] + a.B * f.o_tiles;
     }
     if (mode == 1) {
+      ProfScope ps(PF_TC_PREP, s);
       tc::tc_rowterm_kernel<<<dim3(as[e0].B, rtb.ne), 256, 0, s>>>(rtb);
       ++launched;
     }
+    fb.count = prof_on() ? 1 : 0;
+    // per live tile of one owner pass: S recompute (3 terms x K = 2D) + bias MMA (K = 16) + the 3-term
+    // gradient GEMM (K = 128 streamed rows, N = 2D): (12 D + 32 + 12 D) flops per pair
+    fb.flops_per_tile = (unsigned long long)(24 * ts[e0]->D + 32) * 128 * 128;
+    ProfScope ps(PF_TC_BWD, s);
     if (ts[e0]->D == 32) tc_bwd_launch<32>(fb, s);
     else tc_bwd_launch<64>(fb, s);
     ++launched;
@@ -1778,9 +1725,9 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
 }
 
 inline int tc_pass_backward(const PassArgs& a, const TcLatentBuf& t, void* ws, bool zrows, int mode,
-                            cudaStream_t s) {
+                            bool dense_reverse, cudaStream_t s) {
   const TcLatentBuf* tp = &t;
-  return tc_pass_backward_batch(&a, &tp, 1, ws, zrows, mode, s);
+  return tc_pass_backward_batch(&a, &tp, 1, ws, zrows, mode, dense_reverse, s);
 }
 
 // ------------------------------------------------------------------------------ K2: tmc_factors on tensor cores

@@ -40,6 +40,18 @@ def gather_per_datapoint(local, group=None):
     return torch.cat(parts, dim=0)
 
 
+def data_parallel_estimate(graph, inputs, ws, logp, grads, obj, dlogp=None, group=None, stream=None):
+    """One data-parallel step of the hot path on this rank's shard: the TMC
+    forward and reverse pass of the local datapoints (libtmc; no communication), then the objective
+    obj[0] = sum_b logp[b] (fp64) SUM all-reduced over the group.  graph.B = the local batch."""
+    import torch
+    import paper_1806_08593_b200 as tmc
+    tmc.tmc_forward(graph, inputs, logp, ws, None, stream)
+    tmc.tmc_backward(graph, inputs, ws, dlogp, grads, None, None, stream)
+    torch.sum(logp, dim=0, keepdim=True, out=obj[:1])
+    return reduce_objective(obj, group)
+
+
 def max_over_ranks(values, group=None):
     """In-place MAX all-reduce (device timings: the job time is the slowest rank's)."""
     import torch.distributed as dist

@@ -33,9 +33,10 @@ def upload(torch, wl):
             for i in range(len(wl.parent))]
 
 
-def run_gpu(torch, wl, direction=0, precision=0, dlogp=None, pair=False, grads=True, alpha=1.0):
+def run_gpu(torch, wl, direction=0, precision=0, dlogp=None, pair=False, grads=True, alpha=1.0, flags=0):
     import paper_1806_08593_b200 as tmc
-    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=direction, precision=precision, factor_power=alpha)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B, direction=direction, precision=precision, factor_power=alpha,
+                  flags=flags)
     inp = upload(torch, wl)
     dl = None if dlogp is None else torch.from_numpy(np.asarray(dlogp, np.float64)).cuda()
     logp, gr = tmc.estimate(g, inp, dlogp=dl, grads=grads, pair=pair)
@@ -59,7 +60,22 @@ def rel_err(got, want):
     return max(errs) if errs else 0.0
 
 
+def max_err(got, want):
+    """Per-datapoint element-wise error, max_j |g_j - g*_j| / max_j |g*_j| (A16's element-wise
+    companion): a wrong entry of a low-weight sample cannot hide inside the L2 norm."""
+    errs = []
+    for b in range(want.shape[0]):
+        mw = np.abs(want[b]).max(initial=0.0)
+        if mw < 1e-12:
+            assert np.abs(got[b]).max(initial=0.0) < 1e-6
+            continue
+        errs.append(np.abs(got[b].astype(np.float64) - want[b]).max() / mw)
+    return max(errs) if errs else 0.0
+
+
 def compare(got, ref, b_sel=None, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs"), tag=""):
+    """logp within LOGP_TOL absolute per datapoint; every gradient tensor within GRAD_TOL per
+    datapoint both in relative L2 norm and element-wise against its largest entry."""
     sel = slice(None) if b_sel is None else b_sel
     lg, lr = got["logp"][sel], ref["logp"]
     fin = np.isfinite(lr)
@@ -71,9 +87,14 @@ def compare(got, ref, b_sel=None, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogob
         if k not in ref or k not in got:
             continue
         for i in range(len(ref[k])):
-            e = rel_err(got[k][i][sel], ref[k][i])
-            worst[(k, i)] = e
-            assert e <= GRAD_TOL, f"{tag} latent {i} {k}: rel err {e}"
+            if ref[k][i] is None:
+                continue
+            g = got[k][i][sel]
+            e = rel_err(g, ref[k][i])
+            m = max_err(g, ref[k][i])
+            worst[(k, i)] = max(e, m)
+            assert e <= GRAD_TOL, f"{tag} latent {i} {k}: rel L2 err {e}"
+            assert m <= GRAD_TOL, f"{tag} latent {i} {k}: element-wise err {m}"
     return d.max(initial=0), worst
 
 
@@ -166,15 +187,14 @@ def test_factors_tensor_core_ragged(torch_cuda, name, kw):
 
 
 @pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=300)), ("C4", dict(B=3, K=200)), ("C3", dict(B=2))])
-def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw, monkeypatch):
+def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw):
     """Skipping reverse-pass tiles whose weights are all exactly 0 gives the dense result exactly
     (the skipped P~ are exact zeros); checked with one datapoint's dlogp = 0 as well."""
+    import paper_1806_08593_b200 as tmc
     wl = tw.make_workload(name, **kw)
     w = np.ones(wl.B)
     w[-1] = 0.0
-    monkeypatch.setenv("TMC_DENSE_REVERSE", "1")
-    dense = run_gpu(torch_cuda, wl, dlogp=w)
-    monkeypatch.delenv("TMC_DENSE_REVERSE")
+    dense = run_gpu(torch_cuda, wl, dlogp=w, flags=tmc.TMC_FLAG_DENSE_REVERSE)
     sparse = run_gpu(torch_cuda, wl, dlogp=w)
     for k in dense:
         if k == "logp":
@@ -232,6 +252,7 @@ def test_up_equals_down_on_chain(torch_cuda):
     for k in ("dz", "dmu", "dlogvar"):
         for i in range(len(wl.parent)):
             assert rel_err(d[k][i], u[k][i].astype(np.float64)) < 1e-3
+            assert max_err(d[k][i], u[k][i].astype(np.float64)) < 1e-3
 
 
 @pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=256)), ("C3", dict(B=2, K=640)), ("C2", dict(B=2, K=256)),
@@ -409,7 +430,8 @@ def test_shared_root_exchange(torch_cuda, N, K, world):
             for j, gl in enumerate(lat):
                 if ref[k][gl] is None:
                     continue
-                e = rel_err(gr[j][k].cpu().numpy(), ref[k][gl])
+                gg = gr[j][k].cpu().numpy()
+                e = max(rel_err(gg, ref[k][gl]), max_err(gg, ref[k][gl]))
                 assert e <= GRAD_TOL, (k, gl, e)
 
 

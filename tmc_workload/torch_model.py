@@ -281,3 +281,27 @@ def dregs_step(model: TorchModel, direction: int = 0, precision: int = 0):
     for p_, g_ in list(zip(theta, gt)) + list(zip(phi, gp)):
         res[p_] = torch.zeros_like(p_) if g_ is None else g_
     return L1, L2, res
+
+
+def train_step(model: TorchModel, graph, ws, logp, grads, flat64, seed: int, group=None, stream=None):
+    """One data-parallel training step of the TMC objective on this rank's shard (SURVEY §8a rows
+    a1-a8; §8e): fresh reparameterisation noise (libtmc tmc_sample_normal, keyed by global datapoint
+    id) -> the model's conditionals and log-densities (torch/cuBLAS) -> libtmc tmc_estimate (forward
+    + reverse pass) -> the chain rule into the parameters -> ONE fp64 SUM all-reduce of
+    [objective | every shared-parameter gradient] (flat64 has model.grad_numel + 1 entries).
+    Returns flat64: entry 0 = sum_b logp[b] over all ranks, then the summed parameter gradients."""
+    import paper_1806_08593_b200 as tmc
+    from paper_1806_08593_b200 import parallel
+    torch = model.torch
+    n = model.cfg.n
+    model.zero_grad()
+    model.fresh_noise(seed)
+    f = model.forward()
+    fin = [dict(z=f["z"][i].detach(), mu=f["mu"][i].detach(), logvar=f["logvar"][i].detach(),
+                logq=f["logq"][i].detach(), logobs=None if f["logobs"][i] is None else f["logobs"][i].detach())
+           for i in range(n)]
+    tmc.tmc_estimate(graph, fin, logp, None, grads, ws, stream)
+    model.backward(f, grads)
+    torch.sum(logp, dim=0, keepdim=True, out=flat64[:1])
+    flat64[1:].copy_(model.flat_grads())
+    return parallel.reduce_objective(flat64, group)
