@@ -225,6 +225,45 @@ tmc_status tmc_iwae(const tmc_graph *g, const tmc_latent_in *in, double *logp, c
 tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0, int32_t latent, int32_t K,
                              int32_t D, float *eps, tmc_stream_t stream);
 
+
+/* ---------------------------------------------------------------- general elimination (NEXT-4)
+ * The TMC estimate of an arbitrary (loopy) factor graph over sample indices, PAPER.md "Efficient
+ * averaging" (Fig[factor:loop] P:145-215):
+ *     logp[b] = log( 1/(K_0 ... K_{nvar-1}) sum_{k_0..k_{nvar-1}} prod_j f_j^{kappa_j} )
+ * computed by summing the indices out one at a time in `order`:
+ *     f_new^{kappa'} = 1/K_v sum_{k_v} prod_{j: v in kappa_j} f_j^{kappa_j},  kappa' = (U kappa_j) \ {v}
+ * e.g. Fig[factor:loop]: f_12^{k2 k3} = 1/K1 sum_{k1} f_1^{k1 k2} f_2^{k1 k3}.  Log-domain, online
+ * max (never the appendix's separate maxima, reading A2); the K^{|kappa'|+1} summand of a step is
+ * never stored.  Discrete latents summed out exactly are the special case of one
+ * "sample" per state with uniform Q.
+ *   logf[j]   DEVICE fp32 [B][K_{s0}][K_{s1}][K_{s2}] (row-major in the order of scope[j][.]) = log f_j;
+ *             -inf allowed (a probability-zero event; an all -inf datapoint gives logp = -inf and
+ *             zero gradients).
+ *   arity[j]  1..3; scope[3 j + a] = the a-th index variable of factor j (a < arity[j]).
+ *   order     HOST [nvar] permutation (NULL = 0, 1, ..., nvar-1).  Every factor created by an
+ *             elimination must have <= 3 indices and every index may appear in <= 8 factors at its
+ *             turn, else TMC_ERR_SHAPE (choose another order).  An index no factor contains
+ *             contributes exactly 1 (1/K_v sum_{k_v} 1).
+ * tmc_elim_forward writes logp (DEVICE fp64 [B]) and keeps the intermediate factors in ws.
+ * tmc_elim_backward (after tmc_elim_forward on the same graph, tables and ws, same stream) writes
+ * dlogf[j] = dJ/dlogf_j for J = sum_b dlogp[b] logp[b] (dlogp DEVICE fp64 [B] or NULL = ones; a
+ * NULL entry of dlogf = not wanted) = dlogp[b] times the marginal of kappa_j under the normalised
+ * summand.  Deterministic (no atomics).  B <= 65535. */
+typedef struct {
+  int32_t nvar;           /* index variables k_0 .. k_{nvar-1}, >= 1                            */
+  int32_t B;              /* datapoints (independent problems), >= 0                            */
+  const int32_t *K;       /* HOST [nvar] samples (or states) per index, >= 1                     */
+  int32_t nfac;           /* factors, >= 1                                                      */
+  const int32_t *arity;   /* HOST [nfac] 1..3                                                   */
+  const int32_t *scope;   /* HOST [nfac][3] index variables of each factor (table axis order)   */
+  const int32_t *order;   /* HOST [nvar] elimination order, or NULL                             */
+} tmc_factor_graph;
+size_t tmc_elim_workspace_size(const tmc_factor_graph *g);   /* 0 if the graph/order is invalid */
+tmc_status tmc_elim_forward(const tmc_factor_graph *g, const float *const *logf, double *logp, void *ws,
+                            size_t ws_bytes, tmc_stream_t stream);
+tmc_status tmc_elim_backward(const tmc_factor_graph *g, const float *const *logf, const double *logp, void *ws,
+                             size_t ws_bytes, const double *dlogp, float *const *dlogf, tmc_stream_t stream);
+
 /* Thread-local message describing the last non-OK status on this thread. */
 const char *tmc_last_error(void);
 

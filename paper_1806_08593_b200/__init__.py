@@ -28,7 +28,8 @@ EXPORTS = ["tmc_workspace_size", "tmc_factors", "tmc_forward", "tmc_backward", "
            "tmc_forward_children", "tmc_forward_root", "tmc_sample_normal",
            "tmc_iwae_workspace_size", "tmc_iwae",
            "tmc_estimate_host_workspace_size", "tmc_estimate_host",
-           "tmc_last_error", "tmc_version", "tmc_launch_count", "tmc_profile_begin", "tmc_profile_end"]
+           "tmc_last_error", "tmc_version", "tmc_launch_count", "tmc_profile_begin", "tmc_profile_end",
+           "tmc_elim_workspace_size", "tmc_elim_forward", "tmc_elim_backward"]
 
 
 class TmcError(RuntimeError):
@@ -46,6 +47,12 @@ class tmc_graph(ctypes.Structure):
 
 class tmc_latent_in(ctypes.Structure):
     _fields_ = [(k, ctypes.c_void_p) for k in ("z", "mu", "logvar", "logq", "logobs")]
+
+
+class tmc_factor_graph(ctypes.Structure):
+    _fields_ = [("nvar", ctypes.c_int32), ("B", ctypes.c_int32), ("K", ctypes.POINTER(ctypes.c_int32)),
+                ("nfac", ctypes.c_int32), ("arity", ctypes.POINTER(ctypes.c_int32)),
+                ("scope", ctypes.POINTER(ctypes.c_int32)), ("order", ctypes.POINTER(ctypes.c_int32))]
 
 
 class tmc_profile_entry(ctypes.Structure):
@@ -95,6 +102,13 @@ def load_library(path: str = LIB_PATH):
         lib.tmc_last_error.restype = ctypes.c_char_p
         lib.tmc_version.restype = ctypes.c_int32
         lib.tmc_launch_count.restype = ctypes.c_uint64
+        FG = ctypes.POINTER(tmc_factor_graph)
+        lib.tmc_elim_workspace_size.restype = ctypes.c_size_t
+        lib.tmc_elim_workspace_size.argtypes = [FG]
+        lib.tmc_elim_forward.restype = ctypes.c_int
+        lib.tmc_elim_forward.argtypes = [FG, P, P, P, ctypes.c_size_t, P]
+        lib.tmc_elim_backward.restype = ctypes.c_int
+        lib.tmc_elim_backward.argtypes = [FG, P, P, P, ctypes.c_size_t, P, P, P]
         lib.tmc_profile_begin.restype = ctypes.c_int32
         lib.tmc_profile_begin.argtypes = []
         lib.tmc_profile_end.restype = ctypes.c_int32
@@ -280,6 +294,64 @@ def tmc_version() -> int:
 
 def tmc_launch_count() -> int:
     return load_library().tmc_launch_count()
+
+
+@dataclasses.dataclass
+class FactorGraph:
+    """Host-side metadata of a factor graph over sample indices (tmc_factor_graph, NEXT-4)."""
+    K: Sequence[int]
+    scopes: Sequence[Sequence[int]]
+    B: int
+    order: Optional[Sequence[int]] = None
+
+    def __post_init__(self):
+        nv, nf = len(self.K), len(self.scopes)
+        flat = []
+        for sc in self.scopes:
+            flat += [int(v) for v in sc] + [0] * (3 - len(sc))
+        self._arrs = [(ctypes.c_int32 * nv)(*[int(k) for k in self.K]),
+                      (ctypes.c_int32 * nf)(*[len(sc) for sc in self.scopes]),
+                      (ctypes.c_int32 * max(1, len(flat)))(*flat)]
+        order = None if self.order is None else (ctypes.c_int32 * nv)(*[int(v) for v in self.order])
+        self._order = order
+        self._c = tmc_factor_graph(nv, int(self.B), self._arrs[0], nf, self._arrs[1], self._arrs[2], order)
+
+    def ref(self):
+        return ctypes.byref(self._c)
+
+
+def tmc_elim_workspace_size(fg: FactorGraph) -> int:
+    n = load_library().tmc_elim_workspace_size(fg.ref())
+    if n == 0:
+        raise TmcError(-2, load_library().tmc_last_error().decode())
+    return n
+
+
+def tmc_elim_forward(fg: FactorGraph, logf, logp, ws, stream=None) -> None:
+    """logp (device fp64 [B]) of the factor graph by sequential elimination."""
+    _check(load_library().tmc_elim_forward(fg.ref(), _ptrs(logf), _dp(logp), _dp(ws),
+                                           ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def tmc_elim_backward(fg: FactorGraph, logf, logp, ws, dlogp, dlogf, stream=None) -> None:
+    """dlogf[j] (device fp32, like logf[j]; None = not wanted) = dJ/dlogf_j (factor marginals)."""
+    _check(load_library().tmc_elim_backward(fg.ref(), _ptrs(logf), _dp(logp), _dp(ws),
+                                            ws.numel() * ws.element_size(), _dp(dlogp), _ptrs(dlogf),
+                                            _stream(stream)))
+
+
+def eliminate(fg: FactorGraph, logf, dlogp=None, grads: bool = True, stream=None):
+    """Convenience: (logp, [dlogf_j]) of a factor graph on the device."""
+    import torch
+    dev = logf[0].device
+    ws = torch.empty(tmc_elim_workspace_size(fg), dtype=torch.uint8, device=dev)
+    logp = torch.empty(fg.B, dtype=torch.float64, device=dev)
+    tmc_elim_forward(fg, logf, logp, ws, stream)
+    dl = None
+    if grads:
+        dl = [torch.empty_like(f) for f in logf]
+        tmc_elim_backward(fg, logf, logp, ws, dlogp, dl, stream)
+    return logp, dl
 
 
 def tmc_profile_begin() -> None:

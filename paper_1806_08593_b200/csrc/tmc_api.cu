@@ -14,6 +14,7 @@
 
 #include "../../include/tmc.h"
 #include "tmc_internal.h"
+#include "tmc_elim.cuh"
 #include "tmc_iwae.cuh"
 #include "tmc_sample.cuh"
 #include "tmc_simt.cuh"
@@ -754,6 +755,171 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
 }  // namespace tmc
 
 
+
+// ====================================================================== general elimination (NEXT-4)
+// tmc_elim_*: the TMC estimate of an arbitrary factor graph over sample indices by summing the
+// indices out in a given order; see tmc_elim.cuh and include/tmc.h.
+namespace tmc {
+namespace {
+
+struct ElimFac {
+  std::vector<int> scope;     // variable ids, table layout order
+  long long size = 1;         // entries per datapoint
+  int user = -1;              // index into the caller's logf[] (-1: intermediate in the workspace)
+  size_t tab = 0, off = 0, grad = 0, shift = 0;
+};
+struct ElimStepDesc {
+  int v = 0;
+  std::vector<int> in;        // factor ids
+  int out = -1;
+  std::vector<int> uni;       // union of the input scopes, ascending
+};
+struct ElimPlan {
+  int nvar = 0, B = 0;
+  std::vector<int> K;
+  std::vector<ElimFac> facs;
+  std::vector<ElimStepDesc> steps;
+  std::vector<int> finals;    // 0-index factors left after the last step
+  size_t total = 0;
+};
+
+tmc_status make_elim_plan(const tmc_factor_graph* g, ElimPlan& p) {
+  if (!g) return fail(TMC_ERR_INVALID_ARG, "factor graph is NULL");
+  if (g->nvar <= 0 || g->nfac <= 0) return fail(TMC_ERR_SHAPE, "nvar and nfac must be >= 1");
+  if (g->B < 0 || g->B > 65535) return fail(TMC_ERR_SHAPE, "B must be in [0, 65535]");
+  if (!g->K || !g->arity || !g->scope) return fail(TMC_ERR_INVALID_ARG, "K/arity/scope must be non-NULL");
+  p.nvar = g->nvar;
+  p.B = g->B;
+  p.K.assign(g->K, g->K + g->nvar);
+  for (int v = 0; v < p.nvar; ++v)
+    if (p.K[v] <= 0) return fail(TMC_ERR_SHAPE, "K[" + std::to_string(v) + "] must be >= 1");
+  for (int j = 0; j < g->nfac; ++j) {
+    ElimFac f;
+    const int a = g->arity[j];
+    if (a < 1 || a > elim::kMaxArity) return fail(TMC_ERR_SHAPE, "factor arity must be in [1, 3]");
+    for (int q = 0; q < a; ++q) {
+      const int v = g->scope[j * elim::kMaxArity + q];
+      if (v < 0 || v >= p.nvar) return fail(TMC_ERR_GRAPH, "factor " + std::to_string(j) + ": scope variable out of range");
+      if (std::find(f.scope.begin(), f.scope.end(), v) != f.scope.end())
+        return fail(TMC_ERR_GRAPH, "factor " + std::to_string(j) + ": repeated scope variable");
+      f.scope.push_back(v);
+      f.size *= p.K[v];
+    }
+    if (f.size > INT32_MAX) return fail(TMC_ERR_SHAPE, "factor table too large");
+    f.user = j;
+    p.facs.push_back(f);
+  }
+  std::vector<int> order(p.nvar);
+  if (g->order) order.assign(g->order, g->order + p.nvar);
+  else for (int v = 0; v < p.nvar; ++v) order[v] = v;
+  {
+    std::vector<int> seen(p.nvar, 0);
+    for (int v : order) {
+      if (v < 0 || v >= p.nvar || seen[v]) return fail(TMC_ERR_GRAPH, "order must be a permutation of 0..nvar-1");
+      seen[v] = 1;
+    }
+  }
+  const size_t B = (size_t)std::max(p.B, 1);
+  size_t cur = 0;
+  std::vector<int> live;                       // factor ids not yet consumed
+  for (int j = 0; j < (int)p.facs.size(); ++j) live.push_back(j);
+  for (int v : order) {
+    ElimStepDesc st;
+    st.v = v;
+    std::vector<int> keep;
+    for (int f : live) {
+      const std::vector<int>& sc = p.facs[f].scope;
+      if (std::find(sc.begin(), sc.end(), v) != sc.end()) st.in.push_back(f);
+      else keep.push_back(f);
+    }
+    if (st.in.empty()) continue;              // 1/K_v sum_{k_v} 1 = 1
+    if ((int)st.in.size() > elim::kMaxTouch)
+      return fail(TMC_ERR_SHAPE, "more than 8 factors contain index " + std::to_string(v));
+    for (int f : st.in)
+      for (int u : p.facs[f].scope)
+        if (std::find(st.uni.begin(), st.uni.end(), u) == st.uni.end()) st.uni.push_back(u);
+    std::sort(st.uni.begin(), st.uni.end());
+    if ((int)st.uni.size() > elim::kMaxUnion)
+      return fail(TMC_ERR_SHAPE, "eliminating index " + std::to_string(v) +
+                                     " creates a factor over more than 3 indices (choose another order)");
+    ElimFac nf;
+    for (int u : st.uni)
+      if (u != v) { nf.scope.push_back(u); nf.size *= p.K[u]; }
+    if (nf.size > INT32_MAX) return fail(TMC_ERR_SHAPE, "intermediate factor too large");
+    nf.tab = carve(cur, 4 * B * nf.size);
+    nf.grad = carve(cur, 4 * B * nf.size);
+    nf.off = carve(cur, 8 * B);
+    nf.shift = carve(cur, 4 * B);
+    st.out = (int)p.facs.size();
+    p.facs.push_back(nf);
+    keep.push_back(st.out);
+    live = keep;
+    p.steps.push_back(st);
+  }
+  for (int f : live) {
+    if (!p.facs[f].scope.empty()) return fail(TMC_ERR_GRAPH, "internal: factor left with free indices");
+    p.finals.push_back(f);
+  }
+  if ((int)p.finals.size() > elim::kMaxFinal) return fail(TMC_ERR_SHAPE, "too many disconnected components");
+  p.total = (cur + 255) & ~size_t(255);
+  return TMC_OK;
+}
+
+// Kernel descriptor of step k (pointers resolved against the caller's tables and the workspace).
+elim::Step elim_step_desc(const ElimPlan& p, int k, const float* const* logf, void* ws, float* const* dlogf) {
+  const ElimStepDesc& sd = p.steps[k];
+  elim::Step st{};
+  st.nin = (int)sd.in.size();
+  st.nu = (int)sd.uni.size();
+  st.vpos = (int)(std::find(sd.uni.begin(), sd.uni.end(), sd.v) - sd.uni.begin());
+  st.lnK = std::log((float)p.K[sd.v]);
+  for (int u = 0; u < st.nu; ++u) st.Ku[u] = p.K[sd.uni[u]];
+  auto strides_of = [&](const std::vector<int>& sc, int* out) {
+    for (int u = 0; u < elim::kMaxUnion; ++u) out[u] = 0;
+    long long s = 1;
+    for (int a = (int)sc.size() - 1; a >= 0; --a) {
+      const int u = (int)(std::find(sd.uni.begin(), sd.uni.end(), sc[a]) - sd.uni.begin());
+      out[u] = (int)s;
+      s *= p.K[sc[a]];
+    }
+  };
+  for (int j = 0; j < st.nin; ++j) {
+    const ElimFac& f = p.facs[sd.in[j]];
+    st.tab[j] = f.user >= 0 ? logf[f.user] : at<float>(ws, f.tab);
+    st.toff[j] = f.user >= 0 ? nullptr : at<double>(ws, f.off);
+    st.tsize[j] = f.size;
+    st.tar[j] = (int)f.scope.size();
+    for (int a = 0; a < st.tar[j]; ++a)
+      st.tpos[j][a] = (int)(std::find(sd.uni.begin(), sd.uni.end(), f.scope[a]) - sd.uni.begin());
+    strides_of(f.scope, st.tstride[j]);
+    st.gin[j] = f.user >= 0 ? (dlogf ? dlogf[f.user] : nullptr) : at<float>(ws, f.grad);
+  }
+  const ElimFac& o = p.facs[sd.out];
+  st.out = at<float>(ws, o.tab);
+  st.osize = o.size;
+  strides_of(o.scope, st.ostride);
+  st.ooff = at<double>(ws, o.off);
+  st.shift = at<float>(ws, o.shift);
+  st.gout = at<float>(ws, o.grad);
+  return st;
+}
+
+elim::Final elim_final_desc(const ElimPlan& p, void* ws) {
+  elim::Final f{};
+  f.count = (int)p.finals.size();
+  for (int j = 0; j < f.count; ++j) {
+    const ElimFac& e = p.facs[p.finals[j]];
+    f.res[j] = at<float>(ws, e.tab);
+    f.off[j] = at<double>(ws, e.off);
+    f.grad[j] = at<float>(ws, e.grad);
+  }
+  return f;
+}
+
+}  // namespace
+}  // namespace tmc
+
+
 // ============================================================ host-input streamed estimate (e2e)
 // tmc_estimate_host: the batch is cut into chunks of datapoints (independent problems),
 // chunk c+1's inputs are copied host->device on an internal copy stream into one of two staging
@@ -1136,6 +1302,73 @@ tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double
       cudaEventRecord(hp->done[sl], s);
     }
     return launch_check("tmc_estimate_host");
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+size_t tmc_elim_workspace_size(const tmc_factor_graph* g) {
+  ElimPlan p;
+  if (make_elim_plan(g, p) != TMC_OK) return 0;
+  return std::max<size_t>(p.total, 256);
+}
+
+tmc_status tmc_elim_forward(const tmc_factor_graph* g, const float* const* logf, double* logp, void* ws,
+                            size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    ElimPlan p;
+    tmc_status st = make_elim_plan(g, p);
+    if (st != TMC_OK) return st;
+    if (p.B == 0) return TMC_OK;
+    if (!logf || !logp) return fail(TMC_ERR_INVALID_ARG, "logf / logp is NULL");
+    for (int j = 0; j < g->nfac; ++j)
+      if (!logf[j]) return fail(TMC_ERR_INVALID_ARG, "logf[" + std::to_string(j) + "] is NULL");
+    if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+    if ((st = check_device()) != TMC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ProfScope ps(PF_AUX, s);
+    for (int k = 0; k < (int)p.steps.size(); ++k) {
+      const elim::Step sd = elim_step_desc(p, k, logf, ws, nullptr);
+      dim3 grid((unsigned)((sd.osize + 255) / 256), p.B);
+      elim::elim_step_kernel<<<grid, 256, 0, s>>>(sd);
+      elim::elim_norm_kernel<<<p.B, 256, 0, s>>>(sd);
+      TMC_COUNT_LAUNCH();
+      TMC_COUNT_LAUNCH();
+    }
+    const elim::Final f = elim_final_desc(p, ws);
+    elim::elim_final_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(f, p.B, logp);
+    TMC_COUNT_LAUNCH();
+    return launch_check("tmc_elim_forward");
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
+}
+
+tmc_status tmc_elim_backward(const tmc_factor_graph* g, const float* const* logf, const double* logp, void* ws,
+                             size_t ws_bytes, const double* dlogp, float* const* dlogf, tmc_stream_t stream) {
+  try {
+    ElimPlan p;
+    tmc_status st = make_elim_plan(g, p);
+    if (st != TMC_OK) return st;
+    if (p.B == 0) return TMC_OK;
+    if (!logf || !logp || !dlogf) return fail(TMC_ERR_INVALID_ARG, "logf / logp / dlogf is NULL");
+    if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+    if ((st = check_device()) != TMC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ProfScope ps(PF_AUX, s);
+    const elim::Final f = elim_final_desc(p, ws);
+    elim::elim_final_bwd_kernel<<<(p.B + 127) / 128, 128, 0, s>>>(f, p.B, logp, dlogp);
+    TMC_COUNT_LAUNCH();
+    for (int k = (int)p.steps.size() - 1; k >= 0; --k) {
+      const elim::Step sd = elim_step_desc(p, k, logf, ws, dlogf);
+      for (int j = 0; j < sd.nin; ++j) {
+        if (!sd.gin[j]) continue;
+        dim3 grid((unsigned)((sd.tsize[j] + 255) / 256), p.B);
+        elim::elim_grad_kernel<<<grid, 256, 0, s>>>(sd, j);
+        TMC_COUNT_LAUNCH();
+      }
+    }
+    return launch_check("tmc_elim_backward");
   } catch (...) {
     return fail(TMC_ERR_CUDA, "internal error");
   }

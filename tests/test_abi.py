@@ -90,3 +90,17 @@ def test_extension_call_statuses_without_gpu():
     assert lib.tmc_estimate_host_workspace_size(chain.ref(), 0) == 0
     assert lib.tmc_estimate_host_workspace_size(chain.ref(), 1) > lib.tmc_workspace_size(
         tmc.Graph([-1, 0], [4, 4], [2, 2], B=1).ref())
+
+
+def test_elim_graph_validation():
+    """tmc_elim_*: invalid scopes / orders / intermediates wider than 3 indices are rejected by the
+    host-side plan (workspace query returns 0 + message; nothing is launched)."""
+    ok = tmc.FactorGraph([3, 4, 2, 3], [(0, 1), (0, 2), (1, 3), (2, 3)], 2)
+    assert tmc.tmc_elim_workspace_size(ok) > 0
+    bad = [tmc.FactorGraph([3] * 5, [(0, 1), (0, 2), (0, 3), (0, 4)], 2),       # 4-index intermediate
+           tmc.FactorGraph([3] * 3, [(0, 1), (1, 2)], 2, order=[0, 0, 1]),      # not a permutation
+           tmc.FactorGraph([3] * 3, [(0, 1), (1, 5)], 2),                       # variable out of range
+           tmc.FactorGraph([3] * 3, [(0, 0)], 2)]                               # repeated variable
+    for fg in bad:
+        with pytest.raises(tmc.TmcError):
+            tmc.tmc_elim_workspace_size(fg)
