@@ -24,6 +24,11 @@ template <int MODE>   // 0: SS K-major N=128; 1: SS N=64; 2: TS (A in TMEM) B MN
                       // 8: as 5 with the S MMAs in TS mode (A from TMEM cols 448..511)
                       // 9: as 5 while 20 other warps (5 per SMSP) run an ex2/FADD2 loop (softmax-like issue load)
                       // 10: as 5 with a tcgen05.commit after the S MMAs and two after the gradient MMAs (per tile)
+                      // 11: single-pass reverse tile mix: 12 SS N=128 (S) + 24 TS N=64 (G_row, A = P~ in TMEM)
+                      //     + 24 SS N=64 with A MN-major in shared memory (G_col, A = P~^T)
+                      // 12: as 11 while 4 warps store 64 KB per tile to shared memory (the P~ images)
+                      // 13: packed two-pass gradient: 12 SS N=128 + per K-step P_hi [T_hi|T_lo] (TS N=128)
+                      //     + P_lo T_hi (TS N=64), 8 K-steps
 __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -67,6 +72,43 @@ __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) 
           asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
                        "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+        }
+      }
+    } else if constexpr (MODE == 11 || MODE == 12 || MODE == 13) {
+      constexpr uint32_t idS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idG = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idG2 = (1u << 4) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idC = (1u << 4) | (1u << 15) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 12; ++k) {
+          const uint64_t a = sdesc(A + (k & 3) * 32), b = sdesc(Bs + (k & 3) * 32);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (i % 2) * 128),
+                       "l"(a), "l"(b), "r"(idS), "r"((uint32_t)(k != 0)));
+        }
+        if constexpr (MODE == 13) {
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                         "r"(tmem + ((i + 1) % 2) * 128 + (k & 7) * 8), "l"(b), "r"(idG2), "r"(1u));
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
+                         "r"(tmem + ((i + 1) % 2) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+          }
+        } else {
+          for (int k = 0; k < 24; ++k) {
+            const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                         "r"(tmem + ((i + 1) % 2) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+          }
+          for (int k = 0; k < 24; ++k) {
+            const uint64_t a = sdesc_mn(A + (k & 7) * 2048, 16384), b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 384),
+                         "l"(a), "l"(b), "r"(idC), "r"(1u));
+          }
         }
       }
     } else if constexpr (MODE >= 5 && MODE != 9 || MODE == 9) {
@@ -131,6 +173,15 @@ __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) 
     }
     if (acc.x == 1234.f) out[1023] = 1;
   }
+  if (MODE == 12 && warp != 0) {
+    // 4 warps x 16 KB per tile of 16-byte stores (the P~ hi/lo images of a 128 x 128 tile)
+    uint4* p4 = reinterpret_cast<uint4*>(smem + 49152);
+    const uint4 v = make_uint4(threadIdx.x, 1u, 2u, 3u);
+    for (int i = 0; i < n * 32; ++i) {
+      p4[(i * 32 + (threadIdx.x & 31) + (warp - 1) * 256) & 1023] = v;
+      __syncwarp();
+    }
+  }
   if (MODE == 7 && warp != 0) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* p4 = reinterpret_cast<const float4*>(smem);
@@ -166,7 +217,7 @@ __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) 
 template <int MODE>
 double run(int sms, unsigned long long* d, unsigned long long* h, int n) {
   cudaFuncSetAttribute(bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
-  const int threads = MODE == 9 ? 704 : 128;
+  const int threads = MODE == 9 ? 704 : MODE == 12 ? 160 : 128;
   bench<MODE><<<sms, threads, 70 * 1024>>>(n, d);
   bench<MODE><<<sms, threads, 70 * 1024>>>(n, d);
   cudaDeviceSynchronize();
@@ -185,9 +236,12 @@ int main() {
   printf("{\"clk_per_mma_ss_n128\": %.1f, \"clk_per_mma_ss_n64\": %.1f, \"clk_per_mma_ts_mn_n64\": %.1f, "
          "\"clk_per_mma_ts_mn_n128\": %.1f, \"clk_per_mma_ss_n256\": %.1f, \"clk_per_bwd_tile_mix\": %.1f, "
          "\"clk_per_bwd_tile_mix_with_tmem_traffic\": %.1f, \"clk_per_bwd_tile_mix_with_lds\": %.1f, "
-         "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"clk_per_bwd_tile_mix_busy_smsp\": %.1f, \"clk_per_bwd_tile_mix_3_commits\": %.1f, \"err\": \"%s\"}\n",
+         "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"clk_per_bwd_tile_mix_busy_smsp\": %.1f, \"clk_per_bwd_tile_mix_3_commits\": %.1f, "
+         "\"clk_per_single_pass_tile_mix\": %.1f, \"clk_per_single_pass_tile_mix_with_p_stores\": %.1f, "
+         "\"clk_per_packed_grad_tile_mix\": %.1f, \"err\": \"%s\"}\n",
          run<0>(sms, d, h, n), run<1>(sms, d, h, n), run<2>(sms, d, h, n), run<3>(sms, d, h, n), run<4>(sms, d, h, n),
          run<5>(sms, d, h, 256), run<6>(sms, d, h, 256), run<7>(sms, d, h, 256), run<8>(sms, d, h, 256), run<9>(sms, d, h, 256), run<10>(sms, d, h, 256),
+         run<11>(sms, d, h, 256), run<12>(sms, d, h, 256), run<13>(sms, d, h, 256),
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
