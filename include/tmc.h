@@ -87,8 +87,10 @@ typedef enum {
 
 enum {
   TMC_FLAG_VALIDATE = 1u,      /* scan every input for NaN/+inf first (TMC_ERR_NONFINITE), synchronous   */
-  TMC_FLAG_DENSE_REVERSE = 2u  /* reverse pass computes every tile, including tiles whose pair weights   */
+  TMC_FLAG_DENSE_REVERSE = 2u, /* reverse pass computes every tile, including tiles whose pair weights  */
                                /* are all exactly 0 (skipped by default; identical results, measurement) */
+  TMC_FLAG_TWO_PASS_REVERSE = 4u /* tensor-core reverse pass as two owner passes (S and P~ recomputed per */
+                               /* orientation) instead of the single pass; equal within fp32 rounding   */
 };
 
 typedef struct {

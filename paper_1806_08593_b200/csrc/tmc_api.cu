@@ -20,6 +20,7 @@
 #include "tmc_simt.cuh"
 #include "tmc_small.cuh"
 #include "tmc_tc.cuh"
+#include "tmc_bwd1.cuh"
 
 namespace tmc {
 namespace {
@@ -46,6 +47,7 @@ struct Plan {
   float alpha = 1.f;
   bool dense = false;
   bool dense_reverse = false;      // TMC_FLAG_DENSE_REVERSE: no zero-weight tile skipping
+  bool two_pass_reverse = false;   // TMC_FLAG_TWO_PASS_REVERSE: two owner passes instead of one
   std::vector<int> parent, K, D, Kp;
   std::vector<std::vector<int>> children;
   std::vector<int> roots;
@@ -89,6 +91,7 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   p.alpha = g->factor_power == 0.f ? 1.f : g->factor_power;
   p.dense = dense;
   p.dense_reverse = (g->flags & TMC_FLAG_DENSE_REVERSE) != 0;
+  p.two_pass_reverse = (g->flags & TMC_FLAG_TWO_PASS_REVERSE) != 0;
   p.parent.assign(g->parent, g->parent + g->n);
   p.K.assign(g->K, g->K + g->n);
   p.D.assign(g->D, g->D + g->n);
@@ -659,6 +662,16 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       // row owner (z side): dz_i and pair marginals
       a.gz = g.dz;
       a.pair = dense ? (dlogf ? dlogf[i] : nullptr) : g.pair_marginal;
+      if (p.prec == TMC_PREC_TC && !p.two_pass_reverse && tc_bwd1_ok(p.tc[i], a)) {
+        // single pass: dz, dmu, dlogvar and the parent edge's weights from one S / P~ per tile
+        PassArgs f = a;
+        f.gmu = g.dmu; f.glv = g.dlogvar;
+        f.colsum = p.parent[i] >= 0 ? at<float>(ws, p.e[p.parent[i]].w) : at<float>(ws, p.e[i].colsum);
+        const TcLatentBuf* tp = &p.tc[i];
+        g_launches.fetch_add(tc_pass_backward1_batch(&f, &tp, 1, ws, true, p.dense_reverse, s));
+        pi[i] = at<float>(ws, p.e[i].w);
+        continue;
+      }
       const bool tcb = p.prec == TMC_PREC_TC && tc_bwd_edge_ok(p.tc[i], a);
       if (tcb) g_launches.fetch_add(tc_pass_backward(a, p.tc[i], ws, true, 1, p.dense_reverse, s));
       else launch_pass(a, true, 1, dense != nullptr, s);
@@ -719,12 +732,28 @@ tmc_status backward_impl(const Plan& p, const tmc_latent_in* in, const float* co
       }
       launch_pass_batch(simtRow, 1, dense != nullptr, s);
       launch_pass_batch(simtCol, 2, dense != nullptr, s);
+      // single-pass tensor-core reverse for the eligible edges of the level (one batched launch)
+      {
+        std::vector<PassArgs> fa;
+        std::vector<const TcLatentBuf*> ft;
+        for (size_t k = 0; k < tcI.size(); ++k) {
+          if (p.two_pass_reverse || !tc_bwd1_ok(*tcT[k], rowA[k])) continue;
+          PassArgs f = rowA[k];
+          f.gz = colA[k].gz;
+          f.colsum = colA[k].colsum;
+          fa.push_back(f);
+          ft.push_back(tcT[k]);
+          tcT[k] = nullptr;                    // done
+        }
+        if (!fa.empty())
+          g_launches.fetch_add(tc_pass_backward1_batch(fa.data(), ft.data(), (int)fa.size(), ws, false, p.dense_reverse, s));
+      }
       // batched tensor-core passes, grouped by D (row-owner passes of the level, then column owners)
       for (int Dv : {32, 64}) {
         std::vector<PassArgs> ra, ca;
         std::vector<const TcLatentBuf*> tt;
         for (size_t k = 0; k < tcI.size(); ++k)
-          if (p.D[tcI[k]] == Dv) { ra.push_back(rowA[k]); ca.push_back(colA[k]); tt.push_back(tcT[k]); }
+          if (tcT[k] && p.D[tcI[k]] == Dv) { ra.push_back(rowA[k]); ca.push_back(colA[k]); tt.push_back(tcT[k]); }
         if (ra.empty()) continue;
         g_launches.fetch_add(tc_pass_backward_batch(ra.data(), tt.data(), (int)ra.size(), ws, false, 1, p.dense_reverse, s));
         g_launches.fetch_add(tc_pass_backward_batch(ca.data(), tt.data(), (int)ca.size(), ws, false, 2, p.dense_reverse, s));

@@ -720,3 +720,36 @@ def test_pair_marginal_invariants(torch_cuda, name, kw):
         P = got["pair"][i].astype(np.float64)
         np.testing.assert_allclose(P.sum(axis=(1, 2)), 1.0, rtol=0, atol=1e-4)
         np.testing.assert_allclose(P.sum(axis=2), got["dlogobs"][i], rtol=1e-4, atol=1e-6)   # two passes, fp32
+
+
+@pytest.mark.parametrize("name,kw,direction", [("C3", dict(B=3, K=600), 0), ("C4", dict(B=2, K=520), 0),
+                                               ("C3", dict(B=2, K=2048), 0), ("C4", dict(B=2, K=512), 0),
+                                               ("C3", dict(B=2, K=700), 2)])
+def test_single_pass_reverse_matches_two_pass_and_oracle(torch_cuda, name, kw, direction):
+    """The single-pass tensor-core reverse (one S and one P~ per tile, tc_bwd1_kernel) and the
+    two-owner-pass reverse (TMC_FLAG_TWO_PASS_REVERSE) agree within fp32 rounding, and both match
+    the oracle; both directions (DOWN chain, UP trees / UP on a chain)."""
+    import paper_1806_08593_b200 as tmc
+    wl = tw.make_workload(name, **kw)
+    dl = np.linspace(0.5, 1.5, wl.B)
+    one = run_gpu(torch_cuda, wl, direction=direction, dlogp=dl)
+    two = run_gpu(torch_cuda, wl, direction=direction, dlogp=dl, flags=tmc.TMC_FLAG_TWO_PASS_REVERSE)
+    assert np.array_equal(one["logp"], two["logp"])
+    for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
+        for i in range(len(wl.parent)):
+            assert rel_err(one[k][i], two[k][i].astype(np.float64)) <= 1e-4, (k, i)
+    sample = sorted({0, wl.B - 1})
+    ref = oracle.estimate_workload(tw.make_workload(name, b_ids=sample, **kw), direction="up", dlogp=dl[sample])
+    compare(one, ref, b_sel=sample, tag=f"single-pass {name}")
+
+
+def test_single_pass_reverse_deterministic(torch_cuda):
+    wl = tw.make_workload("C3", B=3, K=520)
+    a = run_gpu(torch_cuda, wl)
+    b = run_gpu(torch_cuda, wl)
+    for k in a:
+        if k == "logp":
+            assert np.array_equal(a[k], b[k])
+        else:
+            for x, y in zip(a[k], b[k]):
+                assert np.array_equal(x, y), k
