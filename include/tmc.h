@@ -89,8 +89,11 @@ enum {
   TMC_FLAG_VALIDATE = 1u,      /* scan every input for NaN/+inf first (TMC_ERR_NONFINITE), synchronous   */
   TMC_FLAG_DENSE_REVERSE = 2u, /* reverse pass computes every tile, including tiles whose pair weights  */
                                /* are all exactly 0 (skipped by default; identical results, measurement) */
-  TMC_FLAG_TWO_PASS_REVERSE = 4u /* tensor-core reverse pass as two owner passes (S and P~ recomputed per */
-                               /* orientation) instead of the single pass; equal within fp32 rounding   */
+  TMC_FLAG_TWO_PASS_REVERSE = 4u, /* tensor-core reverse pass as two owner passes (S and P~ recomputed   */
+                               /* per orientation); equal to the single pass within fp32 rounding        */
+  TMC_FLAG_SINGLE_PASS_REVERSE = 8u /* tensor-core reverse pass as one pass (one S and P~ per tile, D = 32 */
+                               /* edges); the library picks per build which of the two is the default;  */
+                               /* setting both flags is TMC_ERR_INVALID_ARG                              */
 };
 
 typedef struct {
@@ -156,7 +159,9 @@ tmc_status tmc_backward(const tmc_graph *g, const tmc_latent_in *in, const float
                         void *ws, size_t ws_bytes, const double *dlogp, tmc_latent_grad *out,
                         float *const *dlogf_dense, tmc_stream_t stream);
 
-/* tmc_forward + tmc_backward on the fused Gaussian path. */
+/* tmc_forward + tmc_backward on the fused Gaussian path (same results, same workspace).  Small
+ * problems (every K_i <= 64, D_i <= 128, n <= 32, AUTO precision and direction) run as ONE kernel
+ * launch that writes logp and every gradient; the workspace is then left untouched. */
 tmc_status tmc_estimate(const tmc_graph *g, const tmc_latent_in *in, double *logp, const double *dlogp,
                         tmc_latent_grad *out, void *ws, size_t ws_bytes, tmc_stream_t stream);
 

@@ -20,6 +20,7 @@ TMC_PREC_AUTO, TMC_PREC_SIMT, TMC_PREC_TC = 0, 1, 2
 TMC_FLAG_VALIDATE = 1
 TMC_FLAG_DENSE_REVERSE = 2
 TMC_FLAG_TWO_PASS_REVERSE = 4
+TMC_FLAG_SINGLE_PASS_REVERSE = 8
 
 STATUS = {0: "TMC_OK", -1: "TMC_ERR_INVALID_ARG", -2: "TMC_ERR_SHAPE", -3: "TMC_ERR_GRAPH",
           -4: "TMC_ERR_ALIGNMENT", -5: "TMC_ERR_WORKSPACE", -6: "TMC_ERR_UNSUPPORTED_DEVICE",

@@ -24,6 +24,9 @@
 
 namespace tmc {
 namespace {
+// Default tensor-core reverse pass (measured): the two owner passes until the single
+// pass is faster on the bench configurations.
+constexpr bool kDefaultTwoPassReverse = true;
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
@@ -91,7 +94,10 @@ tmc_status make_plan(const tmc_graph* g, bool dense, Plan& p) {
   p.alpha = g->factor_power == 0.f ? 1.f : g->factor_power;
   p.dense = dense;
   p.dense_reverse = (g->flags & TMC_FLAG_DENSE_REVERSE) != 0;
-  p.two_pass_reverse = (g->flags & TMC_FLAG_TWO_PASS_REVERSE) != 0;
+  if ((g->flags & TMC_FLAG_TWO_PASS_REVERSE) && (g->flags & TMC_FLAG_SINGLE_PASS_REVERSE))
+    return fail(TMC_ERR_INVALID_ARG, "TMC_FLAG_TWO_PASS_REVERSE and TMC_FLAG_SINGLE_PASS_REVERSE are exclusive");
+  p.two_pass_reverse = (g->flags & TMC_FLAG_SINGLE_PASS_REVERSE) ? false
+                       : (g->flags & TMC_FLAG_TWO_PASS_REVERSE) ? true : kDefaultTwoPassReverse;
   p.parent.assign(g->parent, g->parent + g->n);
   p.K.assign(g->K, g->K + g->n);
   p.D.assign(g->D, g->D + g->n);
@@ -1091,6 +1097,26 @@ tmc_status tmc_backward(const tmc_graph* g, const tmc_latent_in* in, const float
 
 tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* logp, const double* dlogp,
                         tmc_latent_grad* out, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  try {
+    // small problems: the reverse launch of the small-problem kernel redoes the forward anyway, so the
+    // whole estimate is ONE launch that writes logp and every gradient
+    Plan p;
+    tmc_status st = make_plan(g, false, p);
+    if (st != TMC_OK) return st;
+    if ((st = check_inputs(p, in, nullptr)) != TMC_OK) return st;
+    if (!logp && p.B > 0) return fail(TMC_ERR_INVALID_ARG, "logp is NULL");
+    if (!ws || ws_bytes < p.total) return fail(TMC_ERR_WORKSPACE, "workspace too small: need " + std::to_string(p.total));
+    if ((st = check_device()) != TMC_OK) return st;
+    small::Args A;
+    if (p.B > 0 && !p.any_pad && small_ok(p, false, &A, in, out, logp, dlogp, 1)) {
+      cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+      if (g->flags & TMC_FLAG_VALIDATE)
+        if ((st = validate_inputs(p, in, nullptr, ws, s)) != TMC_OK) return st;
+      return launch_small(A, s);
+    }
+  } catch (...) {
+    return fail(TMC_ERR_CUDA, "internal error");
+  }
   tmc_status st = tmc_forward(g, in, nullptr, logp, ws, ws_bytes, stream);
   if (st != TMC_OK) return st;
   return tmc_backward(g, in, nullptr, ws, ws_bytes, dlogp, out, nullptr, stream);

@@ -44,6 +44,10 @@ def test_workspace_size_and_graph_validation():
     with pytest.raises(tmc.TmcError) as e:           # DOWN on a tree
         tmc.tmc_workspace_size(tmc.Graph([-1, 0, 0], [4, 4, 4], [1, 1, 1], B=1, direction=tmc.TMC_DIR_DOWN))
     assert "chain" in str(e.value)
+    with pytest.raises(tmc.TmcError) as e:           # the two reverse-pass choices are exclusive
+        tmc.tmc_workspace_size(tmc.Graph([-1, 0], [4, 4], [2, 2], B=1, flags=tmc.TMC_FLAG_TWO_PASS_REVERSE
+                                         | tmc.TMC_FLAG_SINGLE_PASS_REVERSE))
+    assert "exclusive" in str(e.value)
 
 
 def _raw_forward(g, inputs, ws_bytes):

@@ -625,6 +625,17 @@ def test_small_problem_kernel(torch_cuda, name, kw):
         got[k] = [gr[i][k].cpu().numpy() for i in range(len(wl.parent))]
     got["pair"] = [gr[i]["pair_marginal"].cpu().numpy() for i in range(len(wl.parent))]
     compare(got, ref, keys=("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair"), tag="small-" + name)
+    # tmc_estimate is ONE launch (§8d C0) with results bit-identical to tmc_forward + tmc_backward
+    logp2 = torch.full_like(logp, float("nan"))
+    gr2 = tmc.alloc_grads(g, pair=True)
+    n0 = tmc.tmc_launch_count()
+    tmc.tmc_estimate(g, inp, logp2, torch.from_numpy(dl).cuda(), gr2, ws)
+    assert tmc.tmc_launch_count() - n0 == 1
+    torch.cuda.synchronize()
+    assert np.array_equal(logp2.cpu().numpy(), got["logp"])
+    for i in range(len(wl.parent)):
+        for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs", "pair_marginal"):
+            assert torch.equal(gr[i][k], gr2[i][k]), (i, k)
 
 
 @pytest.mark.parametrize("name,kw,precision,direction", [
@@ -732,7 +743,7 @@ def test_single_pass_reverse_matches_two_pass_and_oracle(torch_cuda, name, kw, d
     import paper_1806_08593_b200 as tmc
     wl = tw.make_workload(name, **kw)
     dl = np.linspace(0.5, 1.5, wl.B)
-    one = run_gpu(torch_cuda, wl, direction=direction, dlogp=dl)
+    one = run_gpu(torch_cuda, wl, direction=direction, dlogp=dl, flags=tmc.TMC_FLAG_SINGLE_PASS_REVERSE)
     two = run_gpu(torch_cuda, wl, direction=direction, dlogp=dl, flags=tmc.TMC_FLAG_TWO_PASS_REVERSE)
     assert np.array_equal(one["logp"], two["logp"])
     for k in ("dz", "dmu", "dlogvar", "dlogq", "dlogobs"):
@@ -744,9 +755,10 @@ def test_single_pass_reverse_matches_two_pass_and_oracle(torch_cuda, name, kw, d
 
 
 def test_single_pass_reverse_deterministic(torch_cuda):
+    import paper_1806_08593_b200 as tmc
     wl = tw.make_workload("C3", B=3, K=520)
-    a = run_gpu(torch_cuda, wl)
-    b = run_gpu(torch_cuda, wl)
+    a = run_gpu(torch_cuda, wl, flags=tmc.TMC_FLAG_SINGLE_PASS_REVERSE)
+    b = run_gpu(torch_cuda, wl, flags=tmc.TMC_FLAG_SINGLE_PASS_REVERSE)
     for k in a:
         if k == "logp":
             assert np.array_equal(a[k], b[k])
