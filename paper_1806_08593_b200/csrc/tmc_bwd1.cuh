@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  TMC_PROF_T0(_tot);
   if (warp == G::W_PROD) {
     // ---------------- producer: the pair's Y tiles + column-term operands, then the row tiles
     uint32_t v = 0, pa = 0;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
         const uint32_t pb = pair_bits(cmask, p);
         if (!pb || !rmask) continue;
         if (lane == 0) {
-          mbar_wait(y_empty, (pa & 1) ^ 1);
+          TMC_PROF_WAIT(true, 43, mbar_wait(y_empty, (pa & 1) ^ 1));
           mbar_expect_tx(y_full, 2 * G::TILE + 2 * kBxBytes);
           for (int h = 0; h < 2; ++h) {
             const int j = 2 * p + h;
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
           nlive += __popc(pb);
           const uint32_t s = v & 1;
           if (lane == 0) {
-            mbar_wait(&x_empty[s], ((v >> 1) & 1) ^ 1);
+            TMC_PROF_WAIT(true, 44, mbar_wait(&x_empty[s], ((v >> 1) & 1) ^ 1));
             mbar_expect_tx(&x_full[s], G::TILE);
             bulk_g2s(sX + (size_t)s * G::TILE, a.Xt + ((size_t)b * a.r_tiles + i) * G::TILE, G::TILE, &x_full[s]);
           }
@@ -195,16 +196,17 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
     uint32_t gr_uses = 0;                   // G_row accumulator uses (visits)
     auto issue_g = [&](const Pend& q) {
       const uint32_t buf = q.t & 1;
-      mbar_wait(&p_full[buf], (q.t >> 1) & 1);
+      TMC_PROF_WAIT(lane == 0, 26, mbar_wait(&p_full[buf], (q.t >> 1) & 1));
       tc_fence_after();
       // G_col(j) += P~^T X_i  (A = shared P~ image, MN-major; B = X tile MN-major, ones at LBO)
       if (q.first_col) {
-        mbar_wait(&gcol_empty[q.h], ((gc_uses >> q.h) & 1) ^ 1);
+        TMC_PROF_WAIT(lane == 0, 27, mbar_wait(&gcol_empty[q.h], ((gc_uses >> q.h) & 1) ^ 1));
         gc_uses ^= 1u << q.h;
         tc_fence_after();
       }
       const uint32_t gcD = tmem + G::GCOL + q.h * G::GCN;
       const uint32_t xs = xBase + q.xs * G::TILE;
+      TMC_PROF_T0(_gc);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t ko = kk * 2048;
@@ -216,16 +218,18 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
         mma_f16(gcD, aHi, bHi1, IDESC_GC80, 1u);
       }
       mma_commit(pimg_empty);
+      TMC_PROF_END(lane == 0, 46, _gc);
       if (q.last_visit) mma_commit(&x_empty[q.xs]);
       if (q.last_pair) mma_commit(&gcol_full[q.h]);   // the last row tile of the pair: acc h complete
       // G_row(i) += P~ Y_j  (A = P~ in TMEM, B = Y tile MN-major)
       if (q.first_row) {
-        mbar_wait(grow_empty, (gr_uses & 1) ^ 1);
+        TMC_PROF_WAIT(lane == 0, 28, mbar_wait(grow_empty, (gr_uses & 1) ^ 1));
         ++gr_uses;
         tc_fence_after();
       }
       const uint32_t pA = tmem + buf * 128;
       const uint32_t grD = tmem + G::GROW;
+      TMC_PROF_T0(_gr);
       const uint64_t dT = sdesc_mn(yBase + q.h * G::TILE, kAtomBytes);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
@@ -235,6 +239,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
         mma_f16_ts(grD, phi, tlo, IDESC_GR, 1u);
         mma_f16_ts(grD, phi, thi, IDESC_GR, 1u);
       }
+      TMC_PROF_END(lane == 0, 47, _gr);
       if (q.last_visit) mma_commit(grow_full);
       if (q.last_pair && q.last_visit) mma_commit(y_empty);
     };
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
       for (int p = 0; p < npairs; ++p) {
         const uint32_t pb = pair_bits(cmask, p);
         if (!pb || !rmask) continue;
-        mbar_wait(y_full, pa & 1);
+        TMC_PROF_WAIT(lane == 0, 24, mbar_wait(y_full, pa & 1));
         ++pa;
         // the last live visit of this pair
         const int ilast = 63 - __clzll((long long)rmask);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
         for (int i = 0; i < a.r_tiles; ++i) {
           if (!((rmask >> i) & 1)) continue;
           const uint32_t xs = v & 1;
-          mbar_wait(&x_full[xs], (v >> 1) & 1);
+          TMC_PROF_WAIT(lane == 0, 25, mbar_wait(&x_full[xs], (v >> 1) & 1));
           ++v;
           const int hlast = (pb & 2) ? 1 : 0;
           bool first_row = true;
@@ -262,6 +267,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
             // S(i, 2p+h) = X_i Y^T (3-term fp16 split, small terms first) + the column term
             const uint32_t d = tmem + buf * 128;
             const uint64_t dA = sdesc(xBase + xs * G::TILE), dB = sdesc(yBase + h * G::TILE);
+            TMC_PROF_T0(_s);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t o = kk * 32;
@@ -275,6 +281,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
             }
             mma_f16(d, sdesc_bx(smem_u32(sOnesB)), sdesc_bx(smem_u32(sCx) + h * kBxBytes), IDESC_S, 1u);
             mma_commit(&s_full[buf]);
+            TMC_PROF_END(lane == 0, 48, _s);
             if (pend.valid) issue_g(pend);
             pend = Pend{t, xs, (uint32_t)h, first_row ? 1u : 0u, (first_col >> h) & 1u,
                         h == hlast ? 1u : 0u, (i == ilast) ? 1u : 0u, 1u};
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
           for (int h = 0; h < 2; ++h) {
             if (!((pb >> h) & 1)) continue;
             const uint32_t buf = t & 1;
-            mbar_wait(&s_full[buf], (t >> 1) & 1);
+            TMC_PROF_WAIT(warp == 0 && lane == 0, 30, mbar_wait(&s_full[buf], (t >> 1) & 1));
             tc_fence_after();
             const uint32_t ta0 = tmem + lane_off + (uint32_t)(buf * 128 + half * 64);
             // two 32-column quarters, one after the other (keeps the register footprint small)
@@ -345,17 +352,23 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
             for (int c = 0; c < 2; ++c) {
               const uint32_t ta = ta0 + 32 * c;
               uint32_t x[32];
+              TMC_PROF_T0(_l);
               TMC_LD32(ta, x);
               tmem_ld_wait();
+              TMC_PROF_END(warp == 0 && lane == 0, 32, _l);
+              TMC_PROF_T0(_mth);
               uint32_t hi[16], lo[16];
               if (hom > -INFINITY) chunk_math(x, hom2, racc, hi, lo);
               else for (int q = 0; q < 16; ++q) { hi[q] = 0u; lo[q] = 0u; }
+              TMC_PROF_END(warp == 0 && lane == 0, 33, _mth);
+              TMC_PROF_T0(_st);
               TMC_ST16(ta, hi);
               TMC_ST16(ta + 16, lo);
               // the shared image is free once the previous tile's G_col has read it
-              if (c == 0) mbar_wait(pimg_empty, (t & 1) ^ 1);
+              if (c == 0) TMC_PROF_WAIT(warp == 0 && lane == 0, 31, mbar_wait(pimg_empty, (t & 1) ^ 1));
               sts_units(prow_hi, 4 * c, hi);
               sts_units(prow_lo, 4 * c, lo);
+              TMC_PROF_END(warp == 0 && lane == 0, 34, _st);
             }
             tmem_st_wait();
             fence_proxy_async();
@@ -365,7 +378,7 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
             ++t;
           }
           if (a.rowsum) {   // this warp's row sums of the visit -> the epilogue warps
-            mbar_wait(&r_empty[v & 1], ((v >> 1) & 1) ^ 1);
+            TMC_PROF_WAIT(warp == 0 && lane == 0, 35, mbar_wait(&r_empty[v & 1], ((v >> 1) & 1) ^ 1));
             const float2 rr = __fadd2_rn(racc[0], racc[1]);
             sRs[(v & 1) * 256 + half * 128 + m] = rr.x + rr.y;
             __syncwarp();
@@ -399,101 +412,121 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
           const int gm = i * 128 + m;
           const bool rowok = gm < a.Mr;
           const size_t row = ((size_t)b * a.Mr + (rowok ? gm : 0)) * D;
-          mbar_wait(grow_full, gr & 1);
+          const bool first = !((init >> i) & 1);
+          // the row's z and its dz partial so far, loaded before G_row(i) is ready: all 16 loads in
+          // flight at once (one memory latency per visit instead of one per float4); G_row is then
+          // read 8 dimensions at a time (register budget: 64 prefetched + 16 accumulator values)
+          TMC_PROF_T0(_dz);
+          float4 zq[D / 4], dq[D / 4];
+          const bool wz = a.gz && rowok;
+#pragma unroll
+          for (int q = 0; q < D / 4; ++q) {
+            zq[q] = wz ? __ldg(reinterpret_cast<const float4*>(a.z + row) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            dq[q] = (wz && !first) ? __ldcg(reinterpret_cast<const float4*>(a.gz + row) + q)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          const float rprev = (a.rowsum && rowok && !first) ? __ldcg(a.rowsum + (size_t)b * a.Mr + gm) : 0.f;
+          TMC_PROF_END(warp == SMW && lane == 0, 40, _dz);
+          TMC_PROF_WAIT(warp == SMW && lane == 0, 37, mbar_wait(grow_full, gr & 1));
           ++gr;
           tc_fence_after();
-          // dz partial (G1 + 2 z' G0) sgn/2^14 ln 2, 16 dimensions at a time (register pressure)
-          float o[D];
+          // dz partial (G1 + 2 z' G0) sgn/2^14 ln 2 added to the running sum
 #pragma unroll
-          for (int h16 = 0; h16 < D; h16 += 16) {
-            uint32_t g0[16], g1[16];
-            TMC_LD16(tmem + lane_off + G::GROW + h16, g0);       // G0 = sum P~ Y0
-            TMC_LD16(tmem + lane_off + G::GROW + 32 + h16, g1);  // G1 = sum P~ Y1
+          for (int d8 = 0; d8 < D; d8 += 8) {
+            uint32_t g0[8], g1[8];
+            TMC_LD8(tmem + lane_off + G::GROW + d8, g0);       // G0 = sum P~ Y0
+            TMC_LD8(tmem + lane_off + G::GROW + 32 + d8, g1);  // G1 = sum P~ Y1
             tmem_ld_wait();
-            if (h16 + 16 == D) {
+            if (d8 + 8 == D) {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(grow_empty);
             }
 #pragma unroll
-            for (int d4 = 0; d4 < 16; d4 += 4) {
-              float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (a.gz && rowok) z4 = *reinterpret_cast<const float4*>(a.z + row + h16 + d4);
-              const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+            for (int hq = 0; hq < 2; ++hq) {
+              const int d4 = d8 + 4 * hq;
+              const float4 z4 = zq[d4 / 4], p4 = dq[d4 / 4];
+              const float zz[4] = {z4.x, z4.y, z4.z, z4.w}, pp[4] = {p4.x, p4.y, p4.z, p4.w};
+              float o[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                o[h16 + d4 + e] = (__uint_as_float(g1[d4 + e]) + 2.f * (zz[e] - sh[h16 + d4 + e]) *
-                                   __uint_as_float(g0[d4 + e])) * (sc * kLn2);
+                o[e] = pp[e] + (__uint_as_float(g1[4 * hq + e]) + 2.f * (zz[e] - sh[d4 + e]) *
+                                __uint_as_float(g0[4 * hq + e])) * (sc * kLn2);
+              if (wz) *reinterpret_cast<float4*>(a.gz + row + d4) = make_float4(o[0], o[1], o[2], o[3]);
             }
           }
           float rs = 0.f;
           if (a.rowsum) {
-            mbar_wait(&r_full[v & 1], (v >> 1) & 1);
+            TMC_PROF_WAIT(warp == SMW && lane == 0, 38, mbar_wait(&r_full[v & 1], (v >> 1) & 1));
             rs = sRs[(v & 1) * 256 + m] + sRs[(v & 1) * 256 + 128 + m];
             __syncwarp();
             if (lane == 0) mbar_arrive(&r_empty[v & 1]);
           }
           ++v;
-          const bool first = !((init >> i) & 1);
-          if (rowok) {
-            if (a.gz) {
-#pragma unroll
-              for (int d4 = 0; d4 < D; d4 += 4) {
-                float4* dst = reinterpret_cast<float4*>(a.gz + row + d4);
-                float4 q = make_float4(o[d4], o[d4 + 1], o[d4 + 2], o[d4 + 3]);
-                if (!first) {
-                  const float4 p4 = *dst;
-                  q.x += p4.x; q.y += p4.y; q.z += p4.z; q.w += p4.w;
-                }
-                *dst = q;
-              }
-            }
-            if (a.rowsum) a.rowsum[(size_t)b * a.Mr + gm] = (first ? 0.f : a.rowsum[(size_t)b * a.Mr + gm]) + rs * sc;
-          }
+          if (a.rowsum && rowok) a.rowsum[(size_t)b * a.Mr + gm] = rprev + rs * sc;
           init |= 1ull << i;
         }
         // ---- G_col of the pair's two column tiles -> dmu, dlogvar, column sums
         for (int h = 0; h < 2; ++h) {
           const int j = 2 * p + h;
           const bool got = pact && ((pb >> h) & 1);
-          uint32_t c0[32], c1[32], cs[8];
+          const int gc_ = j * 128 + m;
+          const bool colok = gc_ < a.Mc;
+          const size_t row = ((size_t)b * a.Mc + (colok ? gc_ : 0)) * D;
+          // mu / logvar of the column's row, loaded before the accumulator is ready (read-only inputs)
+          const bool ld = got && colok;
+          float4 mq[D / 4], vq[D / 4];
+#pragma unroll
+          for (int q = 0; q < D / 4; ++q) {
+            mq[q] = ld ? __ldg(reinterpret_cast<const float4*>(a.mu + row) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            vq[q] = ld ? __ldg(reinterpret_cast<const float4*>(a.lv + row) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          uint32_t ga = 0;
+          float pi = 0.f;
           if (got) {
-            mbar_wait(&gcol_full[h], (gcp >> h) & 1);
+            TMC_PROF_WAIT(warp == SMW && lane == 0, 39, mbar_wait(&gcol_full[h], (gcp >> h) & 1));
             gcp ^= 1u << h;
             tc_fence_after();
-            const uint32_t ga = tmem + lane_off + G::GCOL + h * G::GCN;
-            TMC_LD32(ga, c0);
-            TMC_LD32(ga + 32, c1);
+            ga = tmem + lane_off + G::GCOL + h * G::GCN;
+            uint32_t cs[8];
             TMC_LD8(ga + 64, cs);
             tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&gcol_empty[h]);
+            pi = __uint_as_float(cs[0]) * sc;
           }
-          const int gc_ = j * 128 + m;
-          if (gc_ >= a.Mc) continue;
-          const size_t row = ((size_t)b * a.Mc + gc_) * D;
-          const float pi = got ? __uint_as_float(cs[0]) * sc : 0.f;
 #pragma unroll
-          for (int d4 = 0; d4 < D; d4 += 4) {
-            float om[4] = {0.f, 0.f, 0.f, 0.f}, ov[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int d8 = 0; d8 < D; d8 += 8) {
+            uint32_t c0[8], c1[8];
             if (got) {
-              const float4 m4 = *reinterpret_cast<const float4*>(a.mu + row + d4);
-              const float4 v4 = *reinterpret_cast<const float4*>(a.lv + row + d4);
-              const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float mp = mm[e] - sh[d4 + e];
-                const float lam = __expf(-vv[e]);
-                const float A1 = __uint_as_float(c1[d4 + e]) * sc, A2 = __uint_as_float(c0[d4 + e]) * sc;
-                om[e] = a.alpha * lam * (A1 - mp * pi);
-                ov[e] = a.alpha * 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+              TMC_LD8(ga + d8, c0);
+              TMC_LD8(ga + 32 + d8, c1);
+              tmem_ld_wait();
+              if (d8 + 8 == D) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&gcol_empty[h]);
               }
             }
-            if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d4) = make_float4(om[0], om[1], om[2], om[3]);
-            if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+#pragma unroll
+            for (int hq = 0; hq < 2; ++hq) {
+              const int d4 = d8 + 4 * hq;
+              float om[4] = {0.f, 0.f, 0.f, 0.f}, ov[4] = {0.f, 0.f, 0.f, 0.f};
+              if (got) {
+                const float4 m4 = mq[d4 / 4], v4 = vq[d4 / 4];
+                const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float mp = mm[e] - sh[d4 + e];
+                  const float lam = __expf(-vv[e]);
+                  const float A1 = __uint_as_float(c1[4 * hq + e]) * sc, A2 = __uint_as_float(c0[4 * hq + e]) * sc;
+                  om[e] = a.alpha * lam * (A1 - mp * pi);
+                  ov[e] = a.alpha * 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+                }
+              }
+              if (colok && a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d4) = make_float4(om[0], om[1], om[2], om[3]);
+              if (colok && a.glv) *reinterpret_cast<float4*>(a.glv + row + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+            }
           }
-          if (a.colsum) a.colsum[(size_t)b * a.Mc + gc_] = pi;
+          if (colok && a.colsum) a.colsum[(size_t)b * a.Mc + gc_] = pi;
         }
       }
       // row tiles that never received a contribution: exact zeros
@@ -508,6 +541,8 @@ __global__ void __launch_bounds__(B1Geo::THREADS, 1) tc_bwd1_kernel(const __grid
       }
     }
   }
+  TMC_PROF_END(lane == 0 && (warp == G::W_PROD || warp == G::W_MMA || warp == 0 || warp == SMW),
+               warp == G::W_PROD ? 45 : warp == G::W_MMA ? 29 : warp == 0 ? 36 : 42, _tot);
   tc_fence_before();
   __syncthreads();
   if (warp == G::W_MMA) {

@@ -46,8 +46,7 @@ def data_parallel_estimate(graph, inputs, ws, logp, grads, obj, dlogp=None, grou
     obj[0] = sum_b logp[b] (fp64) SUM all-reduced over the group.  graph.B = the local batch."""
     import torch
     import paper_1806_08593_b200 as tmc
-    tmc.tmc_forward(graph, inputs, logp, ws, None, stream)
-    tmc.tmc_backward(graph, inputs, ws, dlogp, grads, None, None, stream)
+    tmc.tmc_estimate(graph, inputs, logp, dlogp, grads, ws, stream)
     torch.sum(logp, dim=0, keepdim=True, out=obj[:1])
     return reduce_objective(obj, group)
 
