@@ -27,6 +27,21 @@ def build_variant(name: str, defines, verbose: bool = False) -> str:
     return out
 
 
+def build_debug(force: bool = False, verbose: bool = False) -> str:
+    """libtmc_debug.so: the release library plus an mbarrier-wait deadline (-DTMC_DEBUG_SYNC): a lost
+    pipeline phase traps with the barrier's address instead of hanging the GPU."""
+    out = os.path.join(HERE, "libtmc_debug.so")
+    if not force and os.path.exists(out) and all(os.path.getmtime(s) <= os.path.getmtime(out) for s in sources()):
+        return out
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [NVCC] + FLAGS + ["-DTMC_DEBUG_SYNC", "-o", tmp, SRC]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    os.replace(tmp, out)
+    return out
+
+
 def build_instrumented(verbose: bool = False) -> str:
     """libtmc_instr.so: the same library with per-CTA barrier-wait counters (experiments only)."""
     out = os.path.join(HERE, "libtmc_instr.so")

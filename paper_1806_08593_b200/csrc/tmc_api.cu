@@ -18,8 +18,8 @@
 #include "tmc_iwae.cuh"
 #include "tmc_sample.cuh"
 #include "tmc_simt.cuh"
-#include "tmc_small.cuh"
 #include "tmc_tc.cuh"
+#include "tmc_small.cuh"
 #include "tmc_bwd1.cuh"
 
 namespace tmc {
@@ -468,7 +468,7 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
       L.gz = out[i].dz; L.gmu = out[i].dmu; L.glv = out[i].dlogvar; L.gq = out[i].dlogq; L.go = out[i].dlogobs;
       L.pair = out[i].pair_marginal;
     }
-    L.K = p.K[i]; L.Kp = p.Kp[i]; L.D = p.D[i]; L.parent = p.parent[i];
+    L.K = p.K[i]; L.Kp = p.Kp[i]; L.D = p.D[i]; L.parent = p.parent[i]; L.lnK = std::log((double)p.K[i]);
   }
   A->cache = 0;
   if (small::smem_bytes(*A) > 160 * 1024) return false;
@@ -482,9 +482,9 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
 tmc_status launch_small(const small::Args& A, cudaStream_t s) {
   const size_t smem = small::smem_bytes(A);
   static bool attr[kMaxDevices] = {};
-  ensure_smem_attr(small::small_kernel, 160 * 1024, attr);
+  ensure_smem_attr(small::small_kernel<small::kThreads>, 160 * 1024, attr);
   ProfScope ps(PF_SMALL, s);
-  small::small_kernel<<<A.B, small::kThreads, smem, s>>>(A);
+  small::small_kernel<small::kThreads><<<A.B, small::kThreads, smem, s>>>(A);
   TMC_COUNT_LAUNCH();
   return launch_check("tmc (small-problem kernel)");
 }
@@ -1026,6 +1026,7 @@ size_t tmc_workspace_size(const tmc_graph* g) {
 }
 
 tmc_status tmc_factors(const tmc_graph* g, int32_t i, const tmc_latent_in* in_i, float* logf, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_factors");
   try {
     Plan p;
     tmc_status st = make_plan(g, false, p);
@@ -1053,6 +1054,7 @@ tmc_status tmc_factors(const tmc_graph* g, int32_t i, const tmc_latent_in* in_i,
 
 tmc_status tmc_forward(const tmc_graph* g, const tmc_latent_in* in, const float* const* logf_dense, double* logp,
                        void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_forward");
   try {
     Plan p;
     tmc_status st = make_plan(g, logf_dense != nullptr, p);
@@ -1075,6 +1077,7 @@ tmc_status tmc_forward(const tmc_graph* g, const tmc_latent_in* in, const float*
 tmc_status tmc_backward(const tmc_graph* g, const tmc_latent_in* in, const float* const* logf_dense, void* ws,
                         size_t ws_bytes, const double* dlogp, tmc_latent_grad* out, float* const* dlogf_dense,
                         tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_backward");
   try {
     Plan p;
     tmc_status st = make_plan(g, logf_dense != nullptr, p);
@@ -1097,6 +1100,7 @@ tmc_status tmc_backward(const tmc_graph* g, const tmc_latent_in* in, const float
 
 tmc_status tmc_estimate(const tmc_graph* g, const tmc_latent_in* in, double* logp, const double* dlogp,
                         tmc_latent_grad* out, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_estimate");
   try {
     // small problems: the reverse launch of the small-problem kernel redoes the forward anyway, so the
     // whole estimate is ONE launch that writes logp and every gradient
@@ -1137,6 +1141,7 @@ tmc_status exchange_plan(const tmc_graph* g, const tmc_latent_in* in, void* ws, 
 
 tmc_status tmc_forward_children(const tmc_graph* g, const tmc_latent_in* in, double* root_msg, void* ws,
                                 size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_forward_children");
   try {
     Plan p;
     tmc_status st = exchange_plan(g, in, ws, ws_bytes, p);
@@ -1154,6 +1159,7 @@ tmc_status tmc_forward_children(const tmc_graph* g, const tmc_latent_in* in, dou
 
 tmc_status tmc_forward_root(const tmc_graph* g, const tmc_latent_in* in, const double* root_msg_total, double* logp,
                             void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_forward_root");
   try {
     Plan p;
     tmc_status st = exchange_plan(g, in, ws, ws_bytes, p);
@@ -1169,6 +1175,7 @@ tmc_status tmc_forward_root(const tmc_graph* g, const tmc_latent_in* in, const d
 
 tmc_status tmc_sample_normal(uint64_t seed, uint32_t tag, int32_t B, int64_t b0, int32_t latent, int32_t K, int32_t D,
                              float* eps, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_sample_normal");
   try {
     if (B < 0 || K < 0 || D <= 0 || b0 < 0 || latent < 0) return fail(TMC_ERR_SHAPE, "tmc_sample_normal: bad shape");
     if ((int64_t)K * ((D + 3) / 4) > INT32_MAX || b0 + (int64_t)B > UINT32_MAX)
@@ -1198,6 +1205,7 @@ size_t tmc_iwae_workspace_size(const tmc_graph* g) {
 
 tmc_status tmc_iwae(const tmc_graph* g, const tmc_latent_in* in, double* logp, const double* dlogp,
                     tmc_latent_grad* out, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_iwae");
   try {
     Plan p;
     tmc_status st = make_plan(g, false, p);
@@ -1281,6 +1289,7 @@ size_t tmc_estimate_host_workspace_size(const tmc_graph* g, int32_t chunk) {
 
 tmc_status tmc_estimate_host(const tmc_graph* g, const tmc_latent_in* in, double* logp_host, const double* dlogp_host,
                              tmc_latent_grad* out, int32_t chunk, void* ws, size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_estimate_host");
   try {
     Plan p;
     tmc_status st = make_plan(g, false, p);
@@ -1370,6 +1379,7 @@ size_t tmc_elim_workspace_size(const tmc_factor_graph* g) {
 
 tmc_status tmc_elim_forward(const tmc_factor_graph* g, const float* const* logf, double* logp, void* ws,
                             size_t ws_bytes, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_elim_forward");
   try {
     ElimPlan p;
     tmc_status st = make_elim_plan(g, p);
@@ -1401,6 +1411,7 @@ tmc_status tmc_elim_forward(const tmc_factor_graph* g, const float* const* logf,
 
 tmc_status tmc_elim_backward(const tmc_factor_graph* g, const float* const* logf, const double* logp, void* ws,
                              size_t ws_bytes, const double* dlogp, float* const* dlogf, tmc_stream_t stream) {
+  NvtxRange nvtx_("tmc_elim_backward");
   try {
     ElimPlan p;
     tmc_status st = make_elim_plan(g, p);

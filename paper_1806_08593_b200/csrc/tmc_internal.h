@@ -4,8 +4,19 @@
 #include <mutex>
 #include <vector>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 namespace tmc {
+
+// NVTX ranges (header-only nvtx3; free when no tool is attached): one range per ABI call and one
+// per kernel-family launch scope, so a timeline / `ncu --nvtx` shows which call and which stage
+// every kernel belongs to (launch-gap evidence).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Per-device one-time state (kernel attributes, SM counts): a process may drive several GPUs.
 constexpr int kMaxDevices = 64;
@@ -57,7 +68,8 @@ struct ProfScope {
   int fam;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
-  ProfScope(int fam_, cudaStream_t s_) : fam(fam_), s(s_) {
+  NvtxRange nvtx;
+  ProfScope(int fam_, cudaStream_t s_) : fam(fam_), s(s_), nvtx(prof_name(fam_)) {
     Profiler& p = profiler();
     if (!p.on) return;
     std::lock_guard<std::mutex> lk(p.mu);

@@ -18,7 +18,9 @@ struct Lat {
   const float *z, *mu, *lv, *logq, *logobs;   // inputs
   float *gz, *gmu, *glv, *gq, *go, *pair;      // gradient outputs (any may be NULL)
   int K, Kp, D, parent;
+  double lnK;                                  // ln K (host-computed)
 };
+static_assert(sizeof(Lat) % 16 == 0, "Lat is copied to shared memory in 16-byte units");
 struct Args {
   Lat l[kMaxN];
   int n, B, mode;                              // mode 0: logp only; 1: logp + gradients
@@ -58,9 +60,10 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // F[a*Kp + c] = alpha * (sum_d log N(z[a,d]; mu[c,d], exp(v[c,d])))   (logq enters through h)
+template <int NT>
 __device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
   const int D = L.D;
-  for (int t = threadIdx.x; t < L.K * L.Kp; t += kThreads) {
+  for (int t = threadIdx.x; t < L.K * L.Kp; t += NT) {
     const int a = t / L.Kp, c = t - a * L.Kp;
     float q = 0.f, q2 = 0.f;
     if ((D & 3) == 0) {                       // 16-byte shared-memory loads, two accumulators
@@ -85,23 +88,42 @@ __device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
   }
 }
 
-__device__ __forceinline__ int kkmax(const Args& a) { int m = 1; for (int i = 0; i < a.n; ++i) m = a.l[i].K > m ? a.l[i].K : m; return m; }
-__device__ __forceinline__ int kpmax(const Args& a) { int m = 1; for (int i = 0; i < a.n; ++i) m = a.l[i].Kp > m ? a.l[i].Kp : m; return m; }
+__device__ __forceinline__ int kkmax(const Lat* l, int n) { int m = 1; for (int i = 0; i < n; ++i) m = l[i].K > m ? l[i].K : m; return m; }
+__device__ __forceinline__ int kpmax(const Lat* l, int n) { int m = 1; for (int i = 0; i < n; ++i) m = l[i].Kp > m ? l[i].Kp : m; return m; }
 
-__global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__ Args A) {
+// NT = kThreads threads per CTA (128 measured slower at C0 and C1: more work per thread, same barrier count).
+template <int NT>
+__global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args A) {
+  constexpr int kThreads = NT;
   extern __shared__ __align__(16) unsigned char smraw[];
+  // the per-latent descriptors, copied once from the parameter space in parallel (a chain of
+  // constant-cache misses through the latent loops cost ~6000 clk at C0)
+  __shared__ __align__(16) Lat sL[kMaxN];
   const int b = blockIdx.x, tid = threadIdx.x;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(&A.l[0]);
+    uint4* dst = reinterpret_cast<uint4*>(sL);
+    const int nq = A.n * (int)(sizeof(Lat) / 16);
+    for (int q = tid; q < nq; q += NT) dst[q] = src[q];
+    __syncthreads();
+  }
+#ifdef TMC_INSTRUMENT
+  long long _ph = clock64();
+#define SMALL_MARK(k) do { if (tid == 0) { const long long _n = clock64(); tc::g_tmc_prof[b & 1023][50 + (k)] += _n - _ph; _ph = _n; } } while (0)
+#else
+#define SMALL_MARK(k) do {} while (0)
+#endif
   double* dp = reinterpret_cast<double*>(smraw);
   double* H[kMaxN];
   double* M[kMaxN];
-  for (int i = 0; i < A.n; ++i) { H[i] = dp; dp += A.l[i].K; M[i] = dp; dp += A.l[i].Kp; }
+  for (int i = 0; i < A.n; ++i) { H[i] = dp; dp += sL[i].K; M[i] = dp; dp += sL[i].Kp; }
   if ((reinterpret_cast<uintptr_t>(dp) & 15) != 0) ++dp;      // fp32 region 16-byte aligned (slack in smem_bytes)
   float* fp = reinterpret_cast<float*>(dp);
   float* PI[kMaxN];
   Staged ST[kMaxN];
   auto r4 = [](int x) { return (x + 3) & ~3; };            // matches smem_bytes: 16-byte aligned arrays
   for (int i = 0; i < A.n; ++i) {
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     PI[i] = fp; fp += r4(L.K);
     ST[i].lq = fp; fp += r4(L.K);
     ST[i].lo = fp; fp += r4(L.K);
@@ -113,15 +135,15 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   float* F = fp;
   float* FC[kMaxN];                           // per-latent factor tiles (cache) or the shared scratch
   {
-    float* q = fp + r4(kkmax(A) * kpmax(A));
+    float* q = fp + r4(kkmax(sL, A.n) * kpmax(sL, A.n));
     for (int i = 0; i < A.n; ++i) {
-      if (A.cache) { FC[i] = q; q += r4(A.l[i].K * A.l[i].Kp); }
+      if (A.cache) { FC[i] = q; q += r4(sL[i].K * sL[i].Kp); }
       else FC[i] = F;
     }
   }
   // stage this datapoint's inputs once (all copies in flight together); later phases read shared memory
   for (int i = 0; i < A.n; ++i) {
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     const float* z = L.z + (int64_t)b * L.K * L.D;
     const float* mu = L.mu + (int64_t)b * L.Kp * L.D;
     const float* lv = L.lv + (int64_t)b * L.Kp * L.D;
@@ -132,10 +154,12 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
       if (L.logobs) cp_async4(ST[i].lo + t, L.logobs + (int64_t)b * L.K + t);
     }
   }
+  SMALL_MARK(0);
   cp_async_wait_all();
   __syncthreads();
+  SMALL_MARK(1);
   for (int i = 0; i < A.n; ++i) {              // ldet from the raw log-variances
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     for (int c = tid; c < L.Kp; c += kThreads) {
       float sd = 0.f;
       for (int d = 0; d < L.D; ++d) sd += ST[i].lam[c * L.D + d];
@@ -144,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   }
   // ---- upward: h_i = alpha (logobs_i - logq_i) + sum_children msg; msg_i[c] = LSE_a(F + h) - ln K_i
   for (int i = 0; i < A.n; ++i) {
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     for (int a = tid; a < L.K; a += kThreads) {
       double u = -(double)ST[i].lq[a];
       if (L.logobs) u += (double)ST[i].lo[a];
@@ -153,19 +177,21 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   }
   __syncthreads();
   for (int i = 0; i < A.n; ++i) {              // lam = exp(-v) in place (after ldet read v)
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     for (int t = tid; t < L.Kp * L.D; t += kThreads) ST[i].lam[t] = __expf(-ST[i].lam[t]);
   }
   __syncthreads();
+  SMALL_MARK(2);
   double logp = 0.0;
   for (int i = A.n - 1; i >= 0; --i) {          // parent[i] < i: children come first
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     float* Fi = FC[i];
-    factor(L, ST[i], A.alpha, Fi);
+    factor<NT>(L, ST[i], A.alpha, Fi);
     __syncthreads();
+    SMALL_MARK(3);
     // one warp per column c, lanes over a (K <= 64): warp-shuffle max and sum
     const int warp = tid >> 5, lane = tid & 31;
-    const double lnK = log((double)L.K);
+    const double lnK = L.lnK;
     for (int c = warp; c < L.Kp; c += kThreads / 32) {
       const double x0 = lane < L.K ? (double)Fi[lane * L.Kp + c] + H[i][lane] : -INFINITY;
       const double x1 = lane + 32 < L.K ? (double)Fi[(lane + 32) * L.Kp + c] + H[i][lane + 32] : -INFINITY;
@@ -185,6 +211,7 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
       logp += M[i][0];                          // a root's message is its (K_p = 1) evidence
     }
     __syncthreads();
+    SMALL_MARK(4);
   }
   if (tid == 0) A.logp[b] = logp;
   if (A.mode == 0) return;
@@ -192,18 +219,20 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
   // ---- reverse: pi_root = w softmax(F_root + h_root); P_i[a,c] = pi_p[c] softmax_a(F_i + h_i)[a,c]
   const double w = (logp == -INFINITY) ? 0.0 : (A.dlogp ? A.dlogp[b] : 1.0);
   for (int i = 0; i < A.n; ++i) {
-    const Lat& L = A.l[i];
+    const Lat& L = sL[i];
     float* F = FC[i];                        // the forward sweep's factor tile when cached
-    if (!A.cache) factor(L, ST[i], A.alpha, F);
+    if (!A.cache) factor<NT>(L, ST[i], A.alpha, F);
     __syncthreads();
+    SMALL_MARK(5);
     // P (in place of F): weight of pair (a, c)
     for (int t = tid; t < L.K * L.Kp; t += kThreads) {
       const int a = t / L.Kp, c = t - a * L.Kp;
       const double up = (L.parent >= 0) ? (double)PI[L.parent][c] : w;
-      const double lm = M[i][c] + log((double)L.K);
+      const double lm = M[i][c] + L.lnK;
       F[t] = (up == 0.0 || lm == -INFINITY) ? 0.f : (float)up * __expf((float)((double)F[t] + H[i][a] - lm));
     }
     __syncthreads();
+    SMALL_MARK(6);
     const float al = A.alpha;
     {
       const int warp = tid >> 5, lane = tid & 31;   // one warp per row a, lanes over c
@@ -219,6 +248,7 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
         }
       }
     }
+    SMALL_MARK(7);
     if (L.pair)
       for (int t = tid; t < L.K * L.Kp; t += kThreads) L.pair[(int64_t)b * L.K * L.Kp + t] = al * F[t];
     const int D = L.D;
@@ -247,9 +277,12 @@ __global__ void __launch_bounds__(kThreads) small_kernel(const __grid_constant__
         if (L.gmu) L.gmu[(int64_t)b * L.Kp * D + t] = al * lam * s1;
         if (L.glv) L.glv[(int64_t)b * L.Kp * D + t] = al * 0.5f * (lam * s2 - sp);
       }
+    SMALL_MARK(8);
     __syncthreads();
+    SMALL_MARK(9);
   }
 }
+#undef SMALL_MARK
 
 }  // namespace small
 }  // namespace tmc

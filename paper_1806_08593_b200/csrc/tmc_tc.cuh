@@ -22,6 +22,7 @@
 //   tc_bwd_kernel    (K4): one owner pass of the reverse contraction (below).
 //   tc_factors_kernel(K2): materialised logf (tmc_factors).
 #pragma once
+#include <cstdio>
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
@@ -70,7 +71,34 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-#ifndef TMC_SPIN_WAIT
+#if defined(TMC_DEBUG_SYNC)
+// Debug build (libtmc_debug.so): every mbarrier wait has a deadline of 2^34 SM clocks
+// (~9 s); a pipeline that loses a phase (wrong parity, a missing arrive / commit / expect_tx)
+// reports the barrier and traps, so the launch fails with an error instead of hanging the GPU.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.b32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
+  printf("libtmc (debug): mbarrier wait timed out: block %d thread %d barrier smem 0x%x parity %u\n", blockIdx.x,
+         threadIdx.x, smem_u32(bar), parity);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > (1ll << 34)) mbar_timeout(bar, parity);
+}
+#elif !defined(TMC_SPIN_WAIT)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -820,7 +848,10 @@ struct BGeo {
   static constexpr int TILE = Geo<D>::TILE;
   static constexpr int PART = Geo<D>::PART;
   static constexpr int ATOMS = Geo<D>::ATOMS;
-  static constexpr int ST = (D <= 32) ? 4 : 2;                 // streamed-tile ring depth
+#ifndef TMC_BWD_ST32
+#define TMC_BWD_ST32 4
+#endif
+  static constexpr int ST = (D <= 32) ? TMC_BWD_ST32 : 2;      // streamed-tile ring depth
   static constexpr int SMW = 16;                               // softmax warps (4 per TMEM lane quarter)
   static constexpr int EW = 4;                                 // epilogue warps (1 per TMEM lane quarter)
   static constexpr int THREADS = 32 * (SMW + EW + 2 + TMC_BWD_SPLIT);
