@@ -29,6 +29,9 @@ template <int MODE>   // 0: SS K-major N=128; 1: SS N=64; 2: TS (A in TMEM) B MN
                       // 12: as 11 while 4 warps store 64 KB per tile to shared memory (the P~ images)
                       // 13: packed two-pass gradient: 12 SS N=128 + per K-step P_hi [T_hi|T_lo] (TS N=128)
                       //     + P_lo T_hi (TS N=64), 8 K-steps
+                      // 14: SS, A and B both MN-major, N=64 (the G_col MMA alone); 15: the same at N=80
+                      // 16: tc_bwd1_kernel's exact tile mix: 12 SS N=128 + bias K=16 + 8 x (N=80, 64, 80)
+                      //     A-MN-major SS (G_col) + 24 TS N=64 (G_row)
 __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -72,6 +75,41 @@ __global__ void __launch_bounds__(704, 1) bench(int n, unsigned long long* out) 
           asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 384),
                        "r"(tmem + ((i + 2) % 3) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
+        }
+      }
+    } else if constexpr (MODE == 14 || MODE == 15) {
+      constexpr uint32_t NN = MODE == 14 ? 64u : 80u;
+      constexpr uint32_t idC = (1u << 4) | (1u << 15) | (1u << 16) | ((NN >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < n; ++i) {
+        const uint64_t a = sdesc_mn(A + (i & 7) * 2048, 16384), b = sdesc_mn(Bs + (i & 7) * 2048, 16384);
+        asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                     "l"(a), "l"(b), "r"(idC), "r"(1u));
+      }
+    } else if constexpr (MODE == 16) {
+      constexpr uint32_t idS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idG = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idC64 = (1u << 4) | (1u << 15) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      constexpr uint32_t idC80 = (1u << 4) | (1u << 15) | (1u << 16) | ((80u >> 3) << 17) | ((128u >> 4) << 24);
+      for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 13; ++k) {
+          const uint64_t a = sdesc(A + (k & 3) * 32), b = sdesc(Bs + (k & 3) * 32);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (i % 2) * 128),
+                       "l"(a), "l"(b), "r"(idS), "r"((uint32_t)(k != 0)));
+        }
+        for (int k = 0; k < 24; ++k) {
+          const uint64_t a = sdesc_mn(A + (k & 7) * 2048, 16384), b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+          const uint32_t id = (k % 3 == 1) ? idC64 : idC80;
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                       "l"(a), "l"(b), "r"(id), "r"(1u));
+        }
+        for (int k = 0; k < 24; ++k) {
+          const uint64_t b = sdesc_mn(Bs + (k & 7) * 2048, 16384);
+          asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 416),
+                       "r"(tmem + ((i + 1) % 2) * 128 + (k & 7) * 8), "l"(b), "r"(idG), "r"(1u));
         }
       }
     } else if constexpr (MODE == 11 || MODE == 12 || MODE == 13) {
@@ -238,10 +276,12 @@ int main() {
          "\"clk_per_bwd_tile_mix_with_tmem_traffic\": %.1f, \"clk_per_bwd_tile_mix_with_lds\": %.1f, "
          "\"clk_per_bwd_tile_mix_S_in_TS_mode\": %.1f, \"clk_per_bwd_tile_mix_busy_smsp\": %.1f, \"clk_per_bwd_tile_mix_3_commits\": %.1f, "
          "\"clk_per_single_pass_tile_mix\": %.1f, \"clk_per_single_pass_tile_mix_with_p_stores\": %.1f, "
-         "\"clk_per_packed_grad_tile_mix\": %.1f, \"err\": \"%s\"}\n",
+         "\"clk_per_packed_grad_tile_mix\": %.1f, \"clk_per_mma_ss_amn_n64\": %.1f, \"clk_per_mma_ss_amn_n80\": %.1f, "
+         "\"clk_per_bwd1_exact_tile_mix\": %.1f, \"err\": \"%s\"}\n",
          run<0>(sms, d, h, n), run<1>(sms, d, h, n), run<2>(sms, d, h, n), run<3>(sms, d, h, n), run<4>(sms, d, h, n),
          run<5>(sms, d, h, 256), run<6>(sms, d, h, 256), run<7>(sms, d, h, 256), run<8>(sms, d, h, 256), run<9>(sms, d, h, 256), run<10>(sms, d, h, 256),
          run<11>(sms, d, h, 256), run<12>(sms, d, h, 256), run<13>(sms, d, h, 256),
+         run<14>(sms, d, h, n), run<15>(sms, d, h, n), run<16>(sms, d, h, 256),
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
