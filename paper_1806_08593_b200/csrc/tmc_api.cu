@@ -472,19 +472,24 @@ bool small_ok(const Plan& p, bool dense, small::Args* A, const tmc_latent_in* in
   }
   A->cache = 0;
   if (small::smem_bytes(*A) > 160 * 1024) return false;
-  if (mode == 1) {                            // keep the forward's factor tiles for the reverse sweep if they fit
-    A->cache = 1;
-    if (small::smem_bytes(*A) > 160 * 1024) A->cache = 0;
-  }
+  // keep every latent's factor tile (one factor phase; the reverse sweep reuses them) if they fit
+  A->cache = 1;
+  if (small::smem_bytes(*A) > 160 * 1024) A->cache = 0;
+  small::layout(*A);                          // the shared-memory offsets the kernel addresses by
   return true;
 }
 
 tmc_status launch_small(const small::Args& A, cudaStream_t s) {
   const size_t smem = small::smem_bytes(A);
-  static bool attr[kMaxDevices] = {};
-  ensure_smem_attr(small::small_kernel<small::kThreads>, 160 * 1024, attr);
+  static bool attr[kMaxDevices] = {}, attr2[kMaxDevices] = {};
   ProfScope ps(PF_SMALL, s);
-  small::small_kernel<small::kThreads><<<A.B, small::kThreads, smem, s>>>(A);
+  if (small::large_work(A)) {
+    ensure_smem_attr(small::small_kernel<small::kThreadsLarge>, 160 * 1024, attr2);
+    small::small_kernel<small::kThreadsLarge><<<A.B, small::kThreadsLarge, smem, s>>>(A);
+  } else {
+    ensure_smem_attr(small::small_kernel<small::kThreadsSmall>, 160 * 1024, attr);
+    small::small_kernel<small::kThreadsSmall><<<A.B, small::kThreadsSmall, smem, s>>>(A);
+  }
   TMC_COUNT_LAUNCH();
   return launch_check("tmc (small-problem kernel)");
 }

@@ -12,13 +12,19 @@
 namespace tmc {
 namespace small {
 
-constexpr int kMaxN = 32, kMaxK = 64, kMaxD = 128, kThreads = 256;
+constexpr int kMaxN = 32, kMaxK = 64, kMaxD = 128;
+// Threads per CTA: 256 for tiny graphs, 512 when the per-datapoint work is larger (measured: C0
+// 17.0 vs 17.6 us per launch, C1 30.9 vs 26.6 us; interleaved A/B, scripts/gpu_r2s.sh).
+constexpr int kThreadsSmall = 256, kThreadsLarge = 512, kLargeWork = 1024;
 
 struct Lat {
   const float *z, *mu, *lv, *logq, *logobs;   // inputs
   float *gz, *gmu, *glv, *gq, *go, *pair;      // gradient outputs (any may be NULL)
   int K, Kp, D, parent;
   double lnK;                                  // ln K (host-computed)
+  // byte offsets into the dynamic shared memory (host-computed by layout()): fp64 h, msg; fp32 pi,
+  // logq, logobs, z, mu, lam, ldet, and this latent's factor tile (the shared scratch when not cached)
+  int o_h, o_m, o_pi, o_lq, o_lo, o_z, o_mu, o_lam, o_ldet, o_f, pad_[2];
 };
 static_assert(sizeof(Lat) % 16 == 0, "Lat is copied to shared memory in 16-byte units");
 struct Args {
@@ -30,23 +36,50 @@ struct Args {
   double* logp;
 };
 
-// shared-memory bytes for the graph (per CTA): fp64 h_i, msg_i; fp32 pi_i, the staged inputs
-// z_i [K][D], mu_i and lam_i = exp(-v_i) [Kp][D], ldet_i [Kp] = sum_d v_i, and a K x Kp scratch.
-__host__ inline size_t smem_bytes(const Args& a) {
-  size_t d = 0, f = 0;
-  int kk = 1, kp = 1;
-  auto r4 = [](size_t x) { return (x + 3) & ~size_t(3); };      // every fp32 array 16-byte aligned
+// Shared-memory layout of one CTA (per-latent byte offsets written into A.l[i].o_*; computed on the
+// host so the kernel addresses every array from a shared-memory descriptor instead of building
+// per-thread pointer tables): fp64 h_i [K], msg_i [Kp]; then, 16-byte aligned, fp32 pi_i, logq_i,
+// logobs_i [K], z_i [K][D], mu_i and lam_i = exp(-v_i) [Kp][D], ldet_i [Kp]; a K x Kp scratch; and
+// with A.cache every latent's factor tile.  Returns the bytes.
+__host__ inline size_t layout(Args& a) {
+  size_t off = 0;
   for (int i = 0; i < a.n; ++i) {
-    const Lat& L = a.l[i];
-    d += (size_t)L.K + L.Kp;
-    f += 3 * r4(L.K) + r4((size_t)L.K * L.D) + 2 * r4((size_t)L.Kp * L.D) + r4(L.Kp);   // pi, logq, logobs, z, mu, lam, ldet
+    Lat& L = a.l[i];
+    L.o_h = (int)off; off += 8 * (size_t)L.K;
+    L.o_m = (int)off; off += 8 * (size_t)L.Kp;
+  }
+  off = (off + 15) & ~size_t(15);
+  auto r4 = [](size_t x) { return 4 * ((x + 3) & ~size_t(3)); };   // bytes of a 16-byte aligned fp32 array
+  int kk = 1, kp = 1;
+  for (int i = 0; i < a.n; ++i) {
+    Lat& L = a.l[i];
+    L.o_pi = (int)off; off += r4(L.K);
+    L.o_lq = (int)off; off += r4(L.K);
+    L.o_lo = (int)off; off += r4(L.K);
+    L.o_z = (int)off; off += r4((size_t)L.K * L.D);
+    L.o_mu = (int)off; off += r4((size_t)L.Kp * L.D);
+    L.o_lam = (int)off; off += r4((size_t)L.Kp * L.D);
+    L.o_ldet = (int)off; off += r4(L.Kp);
     kk = L.K > kk ? L.K : kk;
     kp = L.Kp > kp ? L.Kp : kp;
   }
-  f += (size_t)kk * kp;
-  if (a.cache)
-    for (int i = 0; i < a.n; ++i) f += r4((size_t)a.l[i].K * a.l[i].Kp);   // per-latent factor tiles
-  return 8 * d + 4 * f + 64;
+  const size_t scratch = off;
+  off += r4((size_t)kk * kp);
+  for (int i = 0; i < a.n; ++i) {
+    if (a.cache) { a.l[i].o_f = (int)off; off += r4((size_t)a.l[i].K * a.l[i].Kp); }
+    else a.l[i].o_f = (int)scratch;
+  }
+  return off;
+}
+__host__ inline size_t smem_bytes(const Args& a) {
+  Args t = a;
+  return layout(t);
+}
+// sum over latents of the staged elements (K D + Kp D): selects the CTA size
+__host__ inline bool large_work(const Args& a) {
+  long long w = 0;
+  for (int i = 0; i < a.n; ++i) w += (long long)(a.l[i].K + a.l[i].Kp) * a.l[i].D;
+  return w > kLargeWork;
 }
 
 struct Staged { float *z, *mu, *lam, *ldet, *lq, *lo; };
@@ -91,7 +124,7 @@ __device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
 __device__ __forceinline__ int kkmax(const Lat* l, int n) { int m = 1; for (int i = 0; i < n; ++i) m = l[i].K > m ? l[i].K : m; return m; }
 __device__ __forceinline__ int kpmax(const Lat* l, int n) { int m = 1; for (int i = 0; i < n; ++i) m = l[i].Kp > m ? l[i].Kp : m; return m; }
 
-// NT = kThreads threads per CTA (128 measured slower at C0 and C1: more work per thread, same barrier count).
+// NT threads per CTA (128 measured slower at C0 and C1: more work per thread, same barrier count).
 template <int NT>
 __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args A) {
   constexpr int kThreads = NT;
@@ -113,88 +146,77 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
 #else
 #define SMALL_MARK(k) do {} while (0)
 #endif
-  double* dp = reinterpret_cast<double*>(smraw);
-  double* H[kMaxN];
-  double* M[kMaxN];
-  for (int i = 0; i < A.n; ++i) { H[i] = dp; dp += sL[i].K; M[i] = dp; dp += sL[i].Kp; }
-  if ((reinterpret_cast<uintptr_t>(dp) & 15) != 0) ++dp;      // fp32 region 16-byte aligned (slack in smem_bytes)
-  float* fp = reinterpret_cast<float*>(dp);
-  float* PI[kMaxN];
-  Staged ST[kMaxN];
-  auto r4 = [](int x) { return (x + 3) & ~3; };            // matches smem_bytes: 16-byte aligned arrays
-  for (int i = 0; i < A.n; ++i) {
+  // every shared-memory array is addressed from the latent's descriptor (host-computed offsets)
+  auto H = [&](int i) { return reinterpret_cast<double*>(smraw + sL[i].o_h); };
+  auto M = [&](int i) { return reinterpret_cast<double*>(smraw + sL[i].o_m); };
+  auto PI = [&](int i) { return reinterpret_cast<float*>(smraw + sL[i].o_pi); };
+  auto FC = [&](int i) { return reinterpret_cast<float*>(smraw + sL[i].o_f); };
+  auto ST = [&](int i) {
     const Lat& L = sL[i];
-    PI[i] = fp; fp += r4(L.K);
-    ST[i].lq = fp; fp += r4(L.K);
-    ST[i].lo = fp; fp += r4(L.K);
-    ST[i].z = fp; fp += r4(L.K * L.D);
-    ST[i].mu = fp; fp += r4(L.Kp * L.D);
-    ST[i].lam = fp; fp += r4(L.Kp * L.D);
-    ST[i].ldet = fp; fp += r4(L.Kp);
-  }
-  float* F = fp;
-  float* FC[kMaxN];                           // per-latent factor tiles (cache) or the shared scratch
-  {
-    float* q = fp + r4(kkmax(sL, A.n) * kpmax(sL, A.n));
-    for (int i = 0; i < A.n; ++i) {
-      if (A.cache) { FC[i] = q; q += r4(sL[i].K * sL[i].Kp); }
-      else FC[i] = F;
-    }
-  }
+    return Staged{reinterpret_cast<float*>(smraw + L.o_z), reinterpret_cast<float*>(smraw + L.o_mu),
+                  reinterpret_cast<float*>(smraw + L.o_lam), reinterpret_cast<float*>(smraw + L.o_ldet),
+                  reinterpret_cast<float*>(smraw + L.o_lq), reinterpret_cast<float*>(smraw + L.o_lo)};
+  };
   // stage this datapoint's inputs once (all copies in flight together); later phases read shared memory
   for (int i = 0; i < A.n; ++i) {
     const Lat& L = sL[i];
     const float* z = L.z + (int64_t)b * L.K * L.D;
     const float* mu = L.mu + (int64_t)b * L.Kp * L.D;
     const float* lv = L.lv + (int64_t)b * L.Kp * L.D;
-    for (int t = tid; t < L.K * L.D; t += kThreads) cp_async4(ST[i].z + t, z + t);
-    for (int t = tid; t < L.Kp * L.D; t += kThreads) { cp_async4(ST[i].mu + t, mu + t); cp_async4(ST[i].lam + t, lv + t); }
+    for (int t = tid; t < L.K * L.D; t += kThreads) cp_async4(ST(i).z + t, z + t);
+    for (int t = tid; t < L.Kp * L.D; t += kThreads) { cp_async4(ST(i).mu + t, mu + t); cp_async4(ST(i).lam + t, lv + t); }
     for (int t = tid; t < L.K; t += kThreads) {
-      cp_async4(ST[i].lq + t, L.logq + (int64_t)b * L.K + t);
-      if (L.logobs) cp_async4(ST[i].lo + t, L.logobs + (int64_t)b * L.K + t);
+      cp_async4(ST(i).lq + t, L.logq + (int64_t)b * L.K + t);
+      if (L.logobs) cp_async4(ST(i).lo + t, L.logobs + (int64_t)b * L.K + t);
     }
   }
   SMALL_MARK(0);
   cp_async_wait_all();
   __syncthreads();
   SMALL_MARK(1);
-  for (int i = 0; i < A.n; ++i) {              // ldet from the raw log-variances
-    const Lat& L = sL[i];
-    for (int c = tid; c < L.Kp; c += kThreads) {
-      float sd = 0.f;
-      for (int d = 0; d < L.D; ++d) sd += ST[i].lam[c * L.D + d];
-      ST[i].ldet[c] = sd;
-    }
-  }
-  // ---- upward: h_i = alpha (logobs_i - logq_i) + sum_children msg; msg_i[c] = LSE_a(F + h) - ln K_i
+  // ldet = sum_d v, lam = exp(-v) in place (one thread per parameter row), h_i = alpha (logobs - logq)
   for (int i = 0; i < A.n; ++i) {
     const Lat& L = sL[i];
-    for (int a = tid; a < L.K; a += kThreads) {
-      double u = -(double)ST[i].lq[a];
-      if (L.logobs) u += (double)ST[i].lo[a];
-      H[i][a] = (double)A.alpha * u;
+    const Staged S = ST(i);
+    for (int c = tid; c < L.Kp; c += kThreads) {
+      float sd = 0.f;
+      for (int d = 0; d < L.D; ++d) {
+        const float v = S.lam[c * L.D + d];
+        sd += v;
+        S.lam[c * L.D + d] = __expf(-v);
+      }
+      S.ldet[c] = sd;
     }
-  }
-  __syncthreads();
-  for (int i = 0; i < A.n; ++i) {              // lam = exp(-v) in place (after ldet read v)
-    const Lat& L = sL[i];
-    for (int t = tid; t < L.Kp * L.D; t += kThreads) ST[i].lam[t] = __expf(-ST[i].lam[t]);
+    for (int a = tid; a < L.K; a += kThreads) {
+      double u = -(double)S.lq[a];
+      if (L.logobs) u += (double)S.lo[a];
+      H(i)[a] = (double)A.alpha * u;
+    }
   }
   __syncthreads();
   SMALL_MARK(2);
-  double logp = 0.0;
+  // ---- upward: h_i = alpha (logobs_i - logq_i) + sum_children msg; msg_i[c] = LSE_a(F + h) - ln K_i
+  __shared__ double s_logp;
+  if (tid == 0) s_logp = 0.0;
+  if (A.cache) {                                // every factor tile in one phase (they are independent)
+    for (int i = 0; i < A.n; ++i) factor<NT>(sL[i], ST(i), A.alpha, FC(i));
+    __syncthreads();
+  }
   for (int i = A.n - 1; i >= 0; --i) {          // parent[i] < i: children come first
     const Lat& L = sL[i];
-    float* Fi = FC[i];
-    factor<NT>(L, ST[i], A.alpha, Fi);
-    __syncthreads();
+    float* Fi = FC(i);
+    if (!A.cache) {
+      factor<NT>(L, ST(i), A.alpha, Fi);
+      __syncthreads();
+    }
     SMALL_MARK(3);
-    // one warp per column c, lanes over a (K <= 64): warp-shuffle max and sum
+    // one warp per column c, lanes over a (K <= 64): warp-shuffle max and sum; lane 0 adds the
+    // message into the parent's h (each column has one owner warp) or, at a root, into logp
     const int warp = tid >> 5, lane = tid & 31;
     const double lnK = L.lnK;
     for (int c = warp; c < L.Kp; c += kThreads / 32) {
-      const double x0 = lane < L.K ? (double)Fi[lane * L.Kp + c] + H[i][lane] : -INFINITY;
-      const double x1 = lane + 32 < L.K ? (double)Fi[(lane + 32) * L.Kp + c] + H[i][lane + 32] : -INFINITY;
+      const double x0 = lane < L.K ? (double)Fi[lane * L.Kp + c] + H(i)[lane] : -INFINITY;
+      const double x1 = lane + 32 < L.K ? (double)Fi[(lane + 32) * L.Kp + c] + H(i)[lane + 32] : -INFINITY;
       double m = fmax(x0, x1);
 #pragma unroll
       for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -202,84 +224,114 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
       if (m > -INFINITY) s = __expf((float)(x0 - m)) + __expf((float)(x1 - m));
 #pragma unroll
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) M[i][c] = (m > -INFINITY) ? m + (double)__logf(s) - lnK : -INFINITY;
-    }
-    __syncthreads();
-    if (L.parent >= 0) {
-      for (int c = tid; c < L.Kp; c += kThreads) H[L.parent][c] += M[i][c];
-    } else {
-      logp += M[i][0];                          // a root's message is its (K_p = 1) evidence
+      if (lane == 0) {
+        const double msg = (m > -INFINITY) ? m + (double)__logf(s) - lnK : -INFINITY;
+        M(i)[c] = msg;
+        if (L.parent >= 0) H(L.parent)[c] += msg;
+        else s_logp += msg;                     // a root's message is its (K_p = 1) evidence
+      }
     }
     __syncthreads();
     SMALL_MARK(4);
   }
+  const double logp = s_logp;
   if (tid == 0) A.logp[b] = logp;
   if (A.mode == 0) return;
 
   // ---- reverse: pi_root = w softmax(F_root + h_root); P_i[a,c] = pi_p[c] softmax_a(F_i + h_i)[a,c]
   const double w = (logp == -INFINITY) ? 0.0 : (A.dlogp ? A.dlogp[b] : 1.0);
-  for (int i = 0; i < A.n; ++i) {
+  const float al = A.alpha;
+  const int warp = tid >> 5, lane = tid & 31;
+  // P (in place of the factor tile) of the rows a = warp, warp + 8, ... with lanes over c, and the
+  // row sums pi_i[a] = sum_c P[a,c] (the marginal of z_i^a) from the same warp
+  auto pair_rows = [&](int i, float* F) {
     const Lat& L = sL[i];
-    float* F = FC[i];                        // the forward sweep's factor tile when cached
-    if (!A.cache) factor<NT>(L, ST[i], A.alpha, F);
-    __syncthreads();
-    SMALL_MARK(5);
-    // P (in place of F): weight of pair (a, c)
-    for (int t = tid; t < L.K * L.Kp; t += kThreads) {
-      const int a = t / L.Kp, c = t - a * L.Kp;
-      const double up = (L.parent >= 0) ? (double)PI[L.parent][c] : w;
-      const double lm = M[i][c] + L.lnK;
-      F[t] = (up == 0.0 || lm == -INFINITY) ? 0.f : (float)up * __expf((float)((double)F[t] + H[i][a] - lm));
-    }
-    __syncthreads();
-    SMALL_MARK(6);
-    const float al = A.alpha;
-    {
-      const int warp = tid >> 5, lane = tid & 31;   // one warp per row a, lanes over c
-      for (int a = warp; a < L.K; a += kThreads / 32) {
-        float s = 0.f;
-        for (int c = lane; c < L.Kp; c += 32) s += F[a * L.Kp + c];
+    for (int a = warp; a < L.K; a += kThreads / 32) {
+      float s = 0.f;
+      for (int c = lane; c < L.Kp; c += 32) {
+        const double up = (L.parent >= 0) ? (double)PI(L.parent)[c] : w;
+        const double lm = M(i)[c] + L.lnK;
+        const float pv = (up == 0.0 || lm == -INFINITY) ? 0.f
+                         : (float)up * __expf((float)((double)F[a * L.Kp + c] + H(i)[a] - lm));
+        F[a * L.Kp + c] = pv;
+        s += pv;
+      }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-          PI[i][a] = s;
-          if (L.go) L.go[(int64_t)b * L.K + a] = al * s;
-          if (L.gq) L.gq[(int64_t)b * L.K + a] = -al * s;
-        }
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        PI(i)[a] = s;
+        if (L.go) L.go[(int64_t)b * L.K + a] = al * s;
+        if (L.gq) L.gq[(int64_t)b * L.K + a] = -al * s;
       }
     }
-    SMALL_MARK(7);
-    if (L.pair)
-      for (int t = tid; t < L.K * L.Kp; t += kThreads) L.pair[(int64_t)b * L.K * L.Kp + t] = al * F[t];
-    const int D = L.D;
-    const float* z = ST[i].z;
-    const float* mu = ST[i].mu;
-    const float* lamv = ST[i].lam;
-    if (L.gz)
-      for (int t = tid; t < L.K * D; t += kThreads) {          // dz[a,d] = sum_c P (mu - z) lam
-        const int a = t / D, d = t - a * D;
-        float acc = 0.f;
-        for (int c = 0; c < L.Kp; ++c)
-          acc += F[a * L.Kp + c] * (mu[c * D + d] - z[a * D + d]) * lamv[c * D + d];
-        L.gz[(int64_t)b * L.K * D + t] = al * acc;
+  };
+  // The gradients of latent i as items g = 0 .. nz + nm - 1: g < nz = K*D -> dz[a,d] = sum_c P (mu - z) lam;
+  // else dmu, dlogvar of parameter row c (sums over a).  Thread tid takes the items of latent i
+  // with (base + g) % NT == tid, where base counts the items of the latents before i: one
+  // round-robin over every latent's items (small latents share the CTA), with the latent's
+  // constants hoisted out of the item loop.
+  auto grads = [&](int i, int base, const float* F) {
+    const Lat& L = sL[i];
+    const int D = L.D, K = L.K, Kp = L.Kp;
+    const int nz = L.gz ? K * D : 0, nm = (L.gmu || L.glv) ? Kp * D : 0;
+    const Staged S = ST(i);
+    int g = (tid - base) % kThreads;
+    if (g < 0) g += kThreads;
+    for (; g < nz; g += kThreads) {
+      const int a = g / D, d = g - a * D;
+      const float zz = S.z[a * D + d];
+      float acc = 0.f;
+      for (int c = 0; c < Kp; ++c) acc += F[a * Kp + c] * (S.mu[c * D + d] - zz) * S.lam[c * D + d];
+      L.gz[(int64_t)b * K * D + g] = al * acc;
+    }
+    for (g -= nz; g < nm; g += kThreads) {
+      const int c = g / D, d = g - c * D;
+      const float lam = S.lam[c * D + d], mu = S.mu[c * D + d];
+      float s1 = 0.f, s2 = 0.f, sp = 0.f;
+      for (int a = 0; a < K; ++a) {
+        const float pv = F[a * Kp + c], df = S.z[a * D + d] - mu;
+        s1 += pv * df;
+        s2 += pv * df * df;
+        sp += pv;
       }
-    if (L.gmu || L.glv)
-      for (int t = tid; t < L.Kp * D; t += kThreads) {         // dmu, dlogvar of parent sample c
-        const int c = t / D, d = t - c * D;
-        const float lam = lamv[c * D + d];
-        float s1 = 0.f, s2 = 0.f, sp = 0.f;
-        for (int a = 0; a < L.K; ++a) {
-          const float p = F[a * L.Kp + c], df = z[a * D + d] - mu[c * D + d];
-          s1 += p * df;
-          s2 += p * df * df;
-          sp += p;
-        }
-        if (L.gmu) L.gmu[(int64_t)b * L.Kp * D + t] = al * lam * s1;
-        if (L.glv) L.glv[(int64_t)b * L.Kp * D + t] = al * 0.5f * (lam * s2 - sp);
-      }
+      if (L.gmu) L.gmu[(int64_t)b * Kp * D + g] = al * lam * s1;
+      if (L.glv) L.glv[(int64_t)b * Kp * D + g] = al * 0.5f * (lam * s2 - sp);
+    }
+    return nz + nm;
+  };
+  if (A.cache) {
+    // every latent keeps its own tile: the top-down P sweep (one phase per latent), then every
+    // latent's gradients and pair marginals in one flattened phase
+    for (int i = 0; i < A.n; ++i) {
+      pair_rows(i, FC(i));
+      __syncthreads();
+    }
+    SMALL_MARK(6);
+    int base = 0;
+    for (int i = 0; i < A.n; ++i) base += grads(i, base, FC(i));
+    for (int i = 0; i < A.n; ++i) {
+      const Lat& L = sL[i];
+      if (L.pair)
+        for (int t = tid; t < L.K * L.Kp; t += kThreads) L.pair[(int64_t)b * L.K * L.Kp + t] = al * FC(i)[t];
+    }
     SMALL_MARK(8);
-    __syncthreads();
-    SMALL_MARK(9);
+  } else {
+    for (int i = 0; i < A.n; ++i) {
+      const Lat& L = sL[i];
+      float* F = FC(i);
+      factor<NT>(L, ST(i), A.alpha, F);
+      __syncthreads();
+      SMALL_MARK(5);
+      pair_rows(i, F);
+      __syncthreads();
+      SMALL_MARK(7);
+      if (L.pair)
+        for (int t = tid; t < L.K * L.Kp; t += kThreads) L.pair[(int64_t)b * L.K * L.Kp + t] = al * F[t];
+      grads(i, 0, F);
+      SMALL_MARK(8);
+      __syncthreads();                          // the next latent reuses the scratch tile
+      SMALL_MARK(9);
+    }
   }
 }
 #undef SMALL_MARK

@@ -17,7 +17,7 @@
 //                          cp.async.bulk (TMA engine) into a 3-stage mbarrier ring, an MMA warp
 //                          issues tcgen05.mma (+ one K=16 bias MMA) into double-buffered TMEM
 //                          accumulators, 8*RB softmax warps drain TMEM with tcgen05.ld and run the
-//                          online-max log2-sum-exp2 (ex2.approx on MUFU, 3/16 on an FMA polynomial).
+//                          online-max log2-sum-exp2 (ex2.approx on MUFU, 4/16 on a packed FMA polynomial).
 //   tc_rowterm_kernel:     per (datapoint, edge): reverse-pass row terms, their bias tiles, live flags.
 //   tc_bwd_kernel    (K4): one owner pass of the reverse contraction (below).
 //   tc_factors_kernel(K2): materialised logf (tmc_factors).
@@ -237,6 +237,23 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(p, f, 6.9314696e-1f);
   p = fmaf(p, f, 1.0000001f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// The same polynomial on a pair (FADD2 / FFMA2 on packed fp32 pairs, LEA for the exponent add):
+// 12 issue slots per two exponentials instead of ~20.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
+  const float2 M = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, M);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = __ffma2_rn(make_float2(1.3277400e-3f, 1.3277400e-3f), f, make_float2(9.6758800e-3f, 9.6758800e-3f));
+  p = __ffma2_rn(p, f, make_float2(5.5507130e-2f, 5.5507130e-2f));
+  p = __ffma2_rn(p, f, make_float2(2.4022112e-1f, 2.4022112e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.9314696e-1f, 6.9314696e-1f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001f, 1.0000001f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 // Byte offset of element k (fp16 index within the part's row vector) of row r in a tile part
@@ -576,13 +593,13 @@ __device__ __forceinline__ int batch_edge(const Batch& fb, int u) {
   return e;
 }
 
-// 3 of every 16 exponentials of the forward run on the FMA pipe (ex2_poly); DESIGN.md §12c.
-constexpr int kFwdPolyExps = 3;
+// 2 of every 8 exponential pairs of the forward run on the FMA pipe (ex2_poly2, packed); DESIGN.md §12c.
+constexpr int kFwdPolyPairs = 2;
 
 template <int D>
 __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid_constant__ FwdBatch fb) {
   using G = Geo<D>;
-  constexpr int NPOLY = kFwdPolyExps;
+  constexpr int NPOLY2 = kFwdPolyPairs;
   constexpr int RB = G::RB, ST = G::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared window
@@ -751,17 +768,15 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         };
         auto tile_sum = [&](float m) {
-          // NPOLY of every 16 exponentials run on the FMA pipe (ex2_poly), the rest on MUFU;
+          // NPOLY2 of every 8 exponential pairs run on the FMA pipe (ex2_poly2), the rest on MUFU;
           // arguments and partial sums on packed pairs (4 independent float2 accumulators)
           const float2 nm = make_float2(-m, -m);
           float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             const float2 y = __fadd2_rn(x2[q], nm);
-            const int k = 2 * q;
-            const float e0 = ((k & 15) >= 16 - NPOLY) ? ex2_poly(y.x) : ex2(y.x);
-            const float e1 = (((k + 1) & 15) >= 16 - NPOLY) ? ex2_poly(y.y) : ex2(y.y);
-            acc[q & 3] = __fadd2_rn(acc[q & 3], make_float2(e0, e1));
+            const float2 e = ((q & 7) >= 8 - NPOLY2) ? ex2_poly2(y) : make_float2(ex2(y.x), ex2(y.y));
+            acc[q & 3] = __fadd2_rn(acc[q & 3], e);
           }
           const float2 t01 = __fadd2_rn(acc[0], acc[1]), t23 = __fadd2_rn(acc[2], acc[3]);
           const float2 tt = __fadd2_rn(t01, t23);
