@@ -94,9 +94,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // F[a*Kp + c] = alpha * (sum_d log N(z[a,d]; mu[c,d], exp(v[c,d])))   (logq enters through h)
 template <int NT>
-__device__ void factor(const Lat& L, const Staged& S, float alpha, float* F) {
+__device__ void factor(const Lat& L, const Staged& S, float alpha, float* F, int t0 = -1) {
   const int D = L.D;
-  for (int t = threadIdx.x; t < L.K * L.Kp; t += NT) {
+  for (int t = t0 < 0 ? (int)threadIdx.x : t0; t < L.K * L.Kp; t += NT) {
     const int a = t / L.Kp, c = t - a * L.Kp;
     float q = 0.f, q2 = 0.f;
     if ((D & 3) == 0) {                       // 16-byte shared-memory loads, two accumulators
@@ -157,17 +157,28 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
                   reinterpret_cast<float*>(smraw + L.o_lam), reinterpret_cast<float*>(smraw + L.o_ldet),
                   reinterpret_cast<float*>(smraw + L.o_lq), reinterpret_cast<float*>(smraw + L.o_lo)};
   };
+  // Per-latent loops over small item counts start at a rotating thread: thread tid takes the items
+  // t of latent i with (base_i + t) % NT == tid (base_i = the items of the latents before i), so the
+  // latents of a small graph are spread over the CTA instead of all landing on threads 0.. .
+  auto first = [&](int base) { const int f = (tid - base) % kThreads; return f < 0 ? f + kThreads : f; };
   // stage this datapoint's inputs once (all copies in flight together); later phases read shared memory
-  for (int i = 0; i < A.n; ++i) {
-    const Lat& L = sL[i];
-    const float* z = L.z + (int64_t)b * L.K * L.D;
-    const float* mu = L.mu + (int64_t)b * L.Kp * L.D;
-    const float* lv = L.lv + (int64_t)b * L.Kp * L.D;
-    for (int t = tid; t < L.K * L.D; t += kThreads) cp_async4(ST(i).z + t, z + t);
-    for (int t = tid; t < L.Kp * L.D; t += kThreads) { cp_async4(ST(i).mu + t, mu + t); cp_async4(ST(i).lam + t, lv + t); }
-    for (int t = tid; t < L.K; t += kThreads) {
-      cp_async4(ST(i).lq + t, L.logq + (int64_t)b * L.K + t);
-      if (L.logobs) cp_async4(ST(i).lo + t, L.logobs + (int64_t)b * L.K + t);
+  {
+    int base = 0;
+    for (int i = 0; i < A.n; ++i) {
+      const Lat& L = sL[i];
+      const Staged S = ST(i);
+      const float* z = L.z + (int64_t)b * L.K * L.D;
+      const float* mu = L.mu + (int64_t)b * L.Kp * L.D;
+      const float* lv = L.lv + (int64_t)b * L.Kp * L.D;
+      for (int t = first(base); t < L.K * L.D; t += kThreads) cp_async4(S.z + t, z + t);
+      base += L.K * L.D;
+      for (int t = first(base); t < L.Kp * L.D; t += kThreads) { cp_async4(S.mu + t, mu + t); cp_async4(S.lam + t, lv + t); }
+      base += L.Kp * L.D;
+      for (int t = first(base); t < L.K; t += kThreads) {
+        cp_async4(S.lq + t, L.logq + (int64_t)b * L.K + t);
+        if (L.logobs) cp_async4(S.lo + t, L.logobs + (int64_t)b * L.K + t);
+      }
+      base += L.K;
     }
   }
   SMALL_MARK(0);
@@ -175,10 +186,10 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
   __syncthreads();
   SMALL_MARK(1);
   // ldet = sum_d v, lam = exp(-v) in place (one thread per parameter row), h_i = alpha (logobs - logq)
-  for (int i = 0; i < A.n; ++i) {
+  for (int i = 0, base = 0; i < A.n; ++i) {
     const Lat& L = sL[i];
     const Staged S = ST(i);
-    for (int c = tid; c < L.Kp; c += kThreads) {
+    for (int c = first(base); c < L.Kp; c += kThreads) {
       float sd = 0.f;
       for (int d = 0; d < L.D; ++d) {
         const float v = S.lam[c * L.D + d];
@@ -187,11 +198,13 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
       }
       S.ldet[c] = sd;
     }
-    for (int a = tid; a < L.K; a += kThreads) {
+    base += L.Kp;
+    for (int a = first(base); a < L.K; a += kThreads) {
       double u = -(double)S.lq[a];
       if (L.logobs) u += (double)S.lo[a];
       H(i)[a] = (double)A.alpha * u;
     }
+    base += L.K;
   }
   __syncthreads();
   SMALL_MARK(2);
@@ -199,7 +212,10 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
   __shared__ double s_logp;
   if (tid == 0) s_logp = 0.0;
   if (A.cache) {                                // every factor tile in one phase (they are independent)
-    for (int i = 0; i < A.n; ++i) factor<NT>(sL[i], ST(i), A.alpha, FC(i));
+    for (int i = 0, base = 0; i < A.n; ++i) {
+      factor<NT>(sL[i], ST(i), A.alpha, FC(i), first(base));
+      base += sL[i].K * sL[i].Kp;
+    }
     __syncthreads();
   }
   for (int i = A.n - 1; i >= 0; --i) {          // parent[i] < i: children come first
@@ -214,18 +230,20 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
     // message into the parent's h (each column has one owner warp) or, at a root, into logp
     const int warp = tid >> 5, lane = tid & 31;
     const double lnK = L.lnK;
+    // reductions over the lowest W lanes only (W = the power of two covering min(K, 32)); the
+    // max is taken in fp32 (any value near the max stabilises the sum; x - m stays fp64)
+    const int W = L.K >= 32 ? 32 : L.K > 16 ? 32 : L.K > 8 ? 16 : L.K > 4 ? 8 : L.K > 2 ? 4 : 2;
     for (int c = warp; c < L.Kp; c += kThreads / 32) {
       const double x0 = lane < L.K ? (double)Fi[lane * L.Kp + c] + H(i)[lane] : -INFINITY;
       const double x1 = lane + 32 < L.K ? (double)Fi[(lane + 32) * L.Kp + c] + H(i)[lane + 32] : -INFINITY;
-      double m = fmax(x0, x1);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      float s = 0.f;                            // terms <= 1 after the max: fp32 exp and sum
-      if (m > -INFINITY) s = __expf((float)(x0 - m)) + __expf((float)(x1 - m));
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      float mf = (float)fmax(x0, x1);
+      for (int o = W >> 1; o; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+      const double m = (double)mf;
+      float s = 0.f;                            // terms ~<= 1 after the max: fp32 exp and sum
+      if (mf > -INFINITY) s = __expf((float)(x0 - m)) + __expf((float)(x1 - m));
+      for (int o = W >> 1; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {
-        const double msg = (m > -INFINITY) ? m + (double)__logf(s) - lnK : -INFINITY;
+        const double msg = (mf > -INFINITY) ? m + (double)__logf(s) - lnK : -INFINITY;
         M(i)[c] = msg;
         if (L.parent >= 0) H(L.parent)[c] += msg;
         else s_logp += msg;                     // a root's message is its (K_p = 1) evidence
@@ -246,6 +264,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
   // row sums pi_i[a] = sum_c P[a,c] (the marginal of z_i^a) from the same warp
   auto pair_rows = [&](int i, float* F) {
     const Lat& L = sL[i];
+    const int W = L.Kp >= 32 ? 32 : L.Kp > 16 ? 32 : L.Kp > 8 ? 16 : L.Kp > 4 ? 8 : L.Kp > 2 ? 4 : 2;
     for (int a = warp; a < L.K; a += kThreads / 32) {
       float s = 0.f;
       for (int c = lane; c < L.Kp; c += 32) {
@@ -256,8 +275,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const __grid_constant__ Args 
         F[a * L.Kp + c] = pv;
         s += pv;
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      for (int o = W >> 1; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {
         PI(i)[a] = s;
         if (L.go) L.go[(int64_t)b * L.K + a] = al * s;
