@@ -22,7 +22,7 @@ logp = torch.empty(wl.B, dtype=torch.float64, device="cuda")
 grads = tmc.alloc_grads(g)
 lib = tmc.load_library()
 lib.tmc_debug_counters.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
-buf = np.zeros((1024, 32), np.uint64)
+buf = np.zeros((1024, 64), np.uint64)   # g_tmc_prof is [1024][64]
 def counters(clear=1):
     torch.cuda.synchronize()
     assert lib.tmc_debug_counters(buf.ctypes.data, buf.size, clear) == 0
@@ -33,8 +33,8 @@ counters()
 names = {0: "prod.ring_empty", 1: "prod.bias_empty", 2: "prod.own_empty", 14: "prod.total",
          3: "mma.ring_full", 4: "mma.acc_empty", 5: "mma.P_full", 6: "mma.own_full", 7: "mma.G_empty", 12: "mma.total",
          11: "mma.issue_grad", 15: "mma.issue_S", 16: "mma.commit_grad", 17: "mma.fence", 18: "mma.commit_S",
-         8: "smx.acc_full", 9: "smx.bias_full", 10: "smx.G_full", 13: "smx.total",
-         19: "smx.tmem_ld", 20: "smx.tmem_st+arrive", 21: "smx.epilogue", 22: "smx.hom_load"}
+         8: "smx.acc_full", 9: "smx.bias_full", 10: "epi.G_full", 13: "smx.total",
+         32: "bwd.smx0.S_full", 33: "bwd.smx1.S_full", 48: "bwd.smx0.total", 49: "bwd.smx1.total"}
 for phase in ("fwd", "bwd"):
     if phase == "fwd":
         tmc.tmc_forward(g, inp, logp, ws, None, s)
