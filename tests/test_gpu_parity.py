@@ -204,6 +204,41 @@ def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw):
                 assert np.array_equal(x, y), (k, i, np.abs(x - y).max())
 
 
+@pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=300)), ("C4", dict(B=2, K=200)), ("C2", dict(B=3, K=256)),
+                                     ("C0", {}), ("C1", dict(B=4))])
+def test_cuda_graph_replay_matches_eager(torch_cuda, name, kw):
+    """tmc_estimate captured in a CUDA graph (its launches carry programmatic-dependent-launch edges,
+    include/tmc.h) and replayed twice gives the eager results bit for bit."""
+    import paper_1806_08593_b200 as tmc
+    torch = torch_cuda
+    wl = tw.make_workload(name, **kw)
+    g = tmc.Graph(wl.parent, wl.K, wl.D, wl.B)
+    inp = upload(torch, wl)
+    ws = tmc.alloc_workspace(g)
+    logp = torch.empty(wl.B, dtype=torch.float64, device="cuda")
+    grads = tmc.alloc_grads(g)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tmc.tmc_estimate(g, inp, logp, None, grads, ws, side)
+        side.synchronize()
+        eager = [logp.clone()] + [v.clone() for gi in grads for v in gi.values() if v is not None]
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, stream=side):
+            tmc.tmc_estimate(g, inp, logp, None, grads, ws, side)
+    for _ in range(2):
+        logp.zero_()
+        for gi in grads:
+            for v in gi.values():
+                if v is not None:
+                    v.fill_(float("nan"))
+        cg.replay()
+        torch.cuda.synchronize()
+        got = [logp] + [v for gi in grads for v in gi.values() if v is not None]
+        for a, b in zip(eager, got):
+            assert torch.equal(a, b)
+
+
 def test_dlogp_weights_and_zero(torch_cuda):
     wl = tw.make_workload("C4", B=4, K=24)
     w = np.array([1.0, -0.5, 0.0, 2.5])
