@@ -55,7 +55,7 @@ struct Geo {
   static constexpr int TMEM_COLS = RB * 2 * 128;
   static constexpr size_t SMEM = 1024 /*align*/ + (size_t)RB * TILE + (size_t)STAGES * TILE +
                                  (size_t)(STAGES + 1) * 4096 /*bias operand ring + constant ones*/ +
-                                 (size_t)RB * 128 * 8 /*half merge*/ + 512 /*barriers*/;
+                                 2 * (size_t)RB * 128 * 8 /*half merge, unit parity*/ + 512 /*barriers*/;
 };
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -607,8 +607,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
   uint8_t* sB = sA + (size_t)RB * G::TILE;              // ST tiles
   uint8_t* sBx = sB + (size_t)ST * G::TILE;                            // ST x kBxBytes (bias operand ring)
   uint8_t* sAx = sBx + (size_t)ST * kBxBytes;                          // constant ones operand
-  float2* sMerge = reinterpret_cast<float2*>(sAx + kBxBytes);          // RB x 128 (max, sum) of half 1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + RB * 128);
+  float2* sMerge = reinterpret_cast<float2*>(sAx + kBxBytes);          // [2][RB x 128] (max, sum) of half 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMerge + 2 * RB * 128);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 1;
   uint64_t* b_full = bars + 2;            // [ST]
@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
     const int half = sw / (4 * RB);
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
     const int rloc = rb * 128 + quarter * 32 + lane;
-    uint32_t t = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    uint32_t t = 0, ua = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
       TMC_FWD_UNIT();
       float mref = -INFINITY, sum = 0.f;
       for (int j = 0; j < a.b_tiles; ++j, ++t) {
@@ -789,11 +789,15 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
         }
         if (mref > -INFINITY) sum += tile_sum(mref);
       }
-      // merge the two column halves of each row (half 1 -> SMEM -> half 0)
-      if (half == 1) sMerge[rloc] = make_float2(mref, sum);
-      named_bar(1, 32 * G::SOFTMAX_WARPS);
+      // merge the two column halves of each row (half 1 -> SMEM -> half 0): only the two warps
+      // holding the halves of the same rows meet (one named barrier per (row block, lane quarter),
+      // ids 1..4 RB); the merge slots alternate with the unit parity, so half 1 can write the next
+      // unit's slot while half 0 still reads this one (one barrier per unit)
+      float2* mslot = sMerge + (ua & 1) * (RB * 128);
+      if (half == 1) mslot[rloc] = make_float2(mref, sum);
+      named_bar(1 + rb * 4 + quarter, 64);
       if (half == 0) {
-        const float2 o = sMerge[rloc];
+        const float2 o = mslot[rloc];
         const float M = fmaxf(mref, o.x);
         float tot = 0.f;
         if (M > -INFINITY) tot = (mref > -INFINITY ? sum * ex2(mref - M) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - M) : 0.f);
@@ -806,7 +810,6 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           a.out[(size_t)b * a.R + r] = oa + e - a.lnC;
         }
       }
-      named_bar(1, 32 * G::SOFTMAX_WARPS);   // sMerge is reused by the next unit
     }
     TMC_PROF_END(warp == 0 && lane == 0, 13, _tr2);
   }
