@@ -739,6 +739,14 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
     uint32_t t = 0, ua = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
       TMC_FWD_UNIT();
+      // the unit's row terms, loaded now and used after the last tile (their latency is off the
+      // critical path at the unit boundary)
+      const int r = g * RB * 128 + rloc;
+      float ea = 0.f, oa = 0.f;
+      if (half == 0 && r < a.R) {
+        if (a.ell_add) ea = a.ell_add[(size_t)b * a.ell_stride + r];
+        if (a.out_add) oa = a.out_add[(size_t)b * a.R + r];
+      }
       float mref = -INFINITY, sum = 0.f;
       for (int j = 0; j < a.b_tiles; ++j, ++t) {
         const int as = t & 1;
@@ -801,12 +809,10 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
         const float M = fmaxf(mref, o.x);
         float tot = 0.f;
         if (M > -INFINITY) tot = (mref > -INFINITY ? sum * ex2(mref - M) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - M) : 0.f);
-        const int r = g * RB * 128 + rloc;
         if (r < a.R) {
           float e = (tot > 0.f) ? kLn2 * (M + __log2f(tot)) : -INFINITY;
-          if (a.ell_add) e += a.ell_add[(size_t)b * a.ell_stride + r];
+          if (a.ell_add) e += ea;
           a.ell[(size_t)b * a.R + r] = e;
-          const float oa = a.out_add ? a.out_add[(size_t)b * a.R + r] : 0.f;
           a.out[(size_t)b * a.R + r] = oa + e - a.lnC;
         }
       }
@@ -1234,15 +1240,37 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         }
       }
     };
+    // the per-unit global loads (owned-tile live flag, owned row term, streamed-tile live flags) of
+    // unit u + gridDim.x are issued while unit u runs: their latency leaves the unit boundary
+    struct UnitPre { int olv; float ho; int f0, f1; };
+    auto unit_pre = [&](int un) -> UnitPre {
+      UnitPre r{0, 0.f, 0, 0};
+      if (un >= units) return r;
+      const int en = batch_edge(fb, un);
+      const BwdArgs& an = fb.e[en];
+      const int uun = un - fb.ustart[en];
+      const int bn = uun / an.o_tiles, mtn = uun % an.o_tiles;
+      r.olv = olive(an, bn, mtn) ? 1 : 0;
+      r.ho = an.ho[(size_t)bn * an.o_tiles * 128 + mtn * 128 + m];
+      if (an.tlive && an.t_tiles <= 64) {
+        r.f0 = lane < an.t_tiles ? an.tlive[(size_t)bn * an.t_tiles + lane] : 0;
+        r.f1 = lane + 32 < an.t_tiles ? an.tlive[(size_t)bn * an.t_tiles + lane + 32] : 0;
+      }
+      return r;
+    };
+    UnitPre nxt = unit_pre(blockIdx.x);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       TMC_BWD_UNIT();
-      if (!olive(a, b, mt)) continue;
-      const int gm = mt * 128 + m;
-      const float hom = a.ho[(size_t)b * a.o_tiles * 128 + gm] + 14.f;
+      (void)b; (void)mt;
+      const UnitPre cur = nxt;
+      nxt = unit_pre(u + gridDim.x);
+      if (!cur.olv) continue;
+      const float hom = cur.ho + 14.f;
       const float2 hom2 = make_float2(hom, hom);
       float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       TMC_SMX_MARK(4);
-      const uint64_t tm = tmask(a, b);
+      const uint64_t tm = !a.tlive ? ~0ull : a.t_tiles > 64 ? 0ull
+                        : ((uint64_t)__ballot_sync(0xffffffffu, cur.f0) | ((uint64_t)__ballot_sync(0xffffffffu, cur.f1) << 32));
       for (int j = 0; j < a.t_tiles; ++j) {
         if (!live(a, b, tm, j)) continue;
         if (SG == 2 && (int)(t & 1) != grp) { ++t; continue; }
