@@ -227,6 +227,9 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x on the FMA pipe (Cody-Waite range reduction + degree-5 minimax polynomial on [-1/2, 1/2],
 // max relative error 8e-8, below ex2.approx's 2^-22): used to move a fixed share of the forward's
 // exponentials off the MUFU pipe.  Valid for x <= 127 (callers guarantee x <= 8); x < -125 -> ~0.
+#ifndef TMC_FWD_MAXFREE
+#define TMC_FWD_MAXFREE 0   // forward softmax: optimistic tiles without a maximum scan (exact fallback)
+#endif
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -125.f);
   const float t = x + 12582912.f;            // 1.5 * 2^23: round(x) lands in the low mantissa bits
@@ -242,7 +245,11 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // The same polynomial on a pair (FADD2 / FFMA2 on packed fp32 pairs, LEA for the exponent add):
 // 12 issue slots per two exponentials instead of ~20.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
+#if TMC_FWD_MAXFREE
+  x = make_float2(fminf(fmaxf(x.x, -125.f), 126.f), fminf(fmaxf(x.y, -125.f), 126.f));
+#else
   x = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
+#endif
   const float2 M = make_float2(12582912.f, 12582912.f);
   const float2 t = __fadd2_rn(x, M);
   const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
@@ -594,7 +601,10 @@ __device__ __forceinline__ int batch_edge(const Batch& fb, int u) {
 }
 
 // 2 of every 8 exponential pairs of the forward run on the FMA pipe (ex2_poly2, packed); DESIGN.md §12c.
-constexpr int kFwdPolyPairs = 2;
+#ifndef TMC_FWD_NPOLY2
+#define TMC_FWD_NPOLY2 2
+#endif
+constexpr int kFwdPolyPairs = TMC_FWD_NPOLY2;
 
 template <int D>
 __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid_constant__ FwdBatch fb) {
@@ -790,6 +800,17 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           const float2 tt = __fadd2_rn(t01, t23);
           return tt.x + tt.y;
         };
+#if TMC_FWD_MAXFREE
+        // Optimistic tile: sum against the current reference without scanning for the tile maximum.
+        // Any argument above 126 makes the tile sum >= 2^126 (ex2_poly2 clamps there), an argument
+        // that is NaN makes it NaN; both fail the test below and take the exact path.  After the
+        // first reference is set the running sum is >= 1, so terms that underflow are below 2^-126
+        // relative; a reference up to 2^100 below the true maximum costs no fp32 precision.
+        if (mref > -INFINITY) {
+          const float ts = tile_sum(mref);
+          if (ts < 0x1p100f) { sum += ts; continue; }
+        }
+#endif
         const float tmax = tile_max();
         if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
           sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
@@ -864,6 +885,9 @@ struct BwdArgs {
 template <int D>
 #ifndef TMC_BWD_NPOLY
 #define TMC_BWD_NPOLY 0   // reverse-pass softmax: groups (of 8) of 4 exponentials evaluated on the FMA pipe
+#endif
+#ifndef TMC_EPI_PREFETCH
+#define TMC_EPI_PREFETCH 1   // reverse-pass epilogue (D <= 32): owner rows loaded before the accumulator waits
 #endif
 #ifndef TMC_BWD_SPLIT
 #define TMC_BWD_SPLIT 1   // 1: S MMAs and gradient MMAs issued by two warps (see tc_bwd_kernel)
@@ -1368,6 +1392,25 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         }
         continue;
       }
+      // D <= 32: the rows this thread combines with G (z, or mu and logvar) are loaded into registers
+      // before the row-sum and accumulator waits, so the epilogue pays no dependent global-load
+      // latency per 8 features (C4 reverse -1.6%, C3 neutral; at D = 64 the 64 extra registers cost
+      // more than the latency: C2 reverse +3%, so D = 64 keeps the per-8-feature loads).
+      constexpr bool EPI_PRE = TMC_EPI_PREFETCH && D <= 32;
+      const size_t prow = ((size_t)b * a.M + (gm < a.M ? gm : 0)) * D;
+      const float* pA_ = a.owner_z ? a.z : a.mu;
+      float4 pa[8], pb[8];
+      if constexpr (EPI_PRE) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          pa[q] = *reinterpret_cast<const float4*>(pA_ + prow + 4 * q);
+          pb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (!a.owner_z) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pb[q] = *reinterpret_cast<const float4*>(a.lv + prow + 4 * q);
+        }
+      }
       int nl = 0;
       if (a.t_tiles <= 64) {
         nl = __popcll(tmask(a, b) & (a.t_tiles == 64 ? ~0ull : ((1ull << a.t_tiles) - 1)));
@@ -1388,6 +1431,70 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
       const float* sh = a.shift + (size_t)b * D;
       const size_t row = ((size_t)b * a.M + (live ? gm : 0)) * D;
       const uint32_t gaddr = tmem + lane_off + GCOL + gb * GN;
+      if constexpr (EPI_PRE) {
+      {
+        constexpr int c0 = 0;
+#pragma unroll
+        for (int dd = 0; dd < 32; dd += 16) {
+          const int d0 = c0 + dd;
+          uint32_t r0[16], r1[16];
+          TMC_LD16(gaddr + d0, r0);
+          TMC_LD16(gaddr + D + d0, r1);
+          if constexpr (PACKED) {     // + the T_lo column half
+            uint32_t q0[16], q1[16];
+            TMC_LD16(gaddr + 2 * D + d0, q0);
+            TMC_LD16(gaddr + 3 * D + d0, q1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              r0[e] = __float_as_uint(__uint_as_float(r0[e]) + __uint_as_float(q0[e]));
+              r1[e] = __float_as_uint(__uint_as_float(r1[e]) + __uint_as_float(q1[e]));
+            }
+          }
+          tmem_ld_wait();
+          if (live) {
+#pragma unroll
+            for (int d4 = 0; d4 < 16; d4 += 4) {
+              float g0[4], g1[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {   // no live streamed tile: the accumulator was never written
+                g0[e] = nl ? __uint_as_float(r0[d4 + e]) : 0.f;
+                g1[e] = nl ? __uint_as_float(r1[d4 + e]) : 0.f;
+              }
+              const float4 a4 = pa[(dd + d4) >> 2];
+              const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+              if (a.owner_z) {
+                // G = sum P (Y = [-lam/2, lam mu'] log2e): dz = sum P lam (mu' - z') = (G1 + 2 z' G0) / log2e
+                if (a.gz) {
+                  float o[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float zp = av[e] - sh[d0 + d4 + e];
+                    o[e] = (g1[e] + 2.f * zp * g0[e]) * (sc * kLn2);
+                  }
+                  *reinterpret_cast<float4*>(a.gz + row + d0 + d4) = make_float4(o[0], o[1], o[2], o[3]);
+                }
+              } else {
+                // G = sum P (X = [z'^2, z']): A2 = sum P z'^2, A1 = sum P z'
+                const float4 v4 = pb[(dd + d4) >> 2];
+                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                float om[4], ov[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float mp = av[e] - sh[d0 + d4 + e];
+                  const float lam = __expf(-vv[e]);
+                  const float A1 = g1[e] * sc, A2 = g0[e] * sc;
+                  om[e] = a.alpha * lam * (A1 - mp * pi);
+                  ov[e] = a.alpha * 0.5f * (lam * (A2 - 2.f * mp * A1 + mp * mp * pi) - pi);
+                }
+                if (a.gmu) *reinterpret_cast<float4*>(a.gmu + row + d0 + d4) = make_float4(om[0], om[1], om[2], om[3]);
+                if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d0 + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+              }
+            }
+          }
+        }
+      }
+      } else {
 #pragma unroll 1
       for (int d0 = 0; d0 < D; d0 += 8) {
         uint32_t r0[8], r1[8];
@@ -1448,6 +1555,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
             if (a.glv) *reinterpret_cast<float4*>(a.glv + row + d0 + d4) = make_float4(ov[0], ov[1], ov[2], ov[3]);
           }
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -1522,7 +1630,10 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
 // The reverse pass's gradient GEMM uses the 3-term fp16 product (P_lo T_hi + P_hi T_lo + P_hi T_hi,
 // DESIGN.md §6) and 8 wide softmax warps (SG = 3).  Zero-weight tile skipping is exact; the graph
 // flag TMC_FLAG_DENSE_REVERSE disables it (every tile computed, for measurement).
-constexpr int kGradTerms = 3;
+#ifndef TMC_GRAD_TERMS
+#define TMC_GRAD_TERMS 3
+#endif
+constexpr int kGradTerms = TMC_GRAD_TERMS;
 constexpr int kBwdGroups = 3;
 
 struct TcLatentBuf {
@@ -1792,7 +1903,7 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
     fb.count = prof_on() ? 1 : 0;
     // per live tile of one owner pass: S recompute (3 terms x K = 2D) + bias MMA (K = 16) + the 3-term
     // gradient GEMM (K = 128 streamed rows, N = 2D): (12 D + 32 + 12 D) flops per pair
-    fb.flops_per_tile = (unsigned long long)(24 * ts[e0]->D + 32) * 128 * 128;
+    fb.flops_per_tile = (unsigned long long)((12 + 4 * (kGradTerms > 3 ? 2 : kGradTerms)) * ts[e0]->D + 32) * 128 * 128;
     ProfScope ps(PF_TC_BWD, s);
     if (ts[e0]->D == 32) tc_bwd_launch<32>(fb, s);
     else tc_bwd_launch<64>(fb, s);
