@@ -227,9 +227,6 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x on the FMA pipe (Cody-Waite range reduction + degree-5 minimax polynomial on [-1/2, 1/2],
 // max relative error 8e-8, below ex2.approx's 2^-22): used to move a fixed share of the forward's
 // exponentials off the MUFU pipe.  Valid for x <= 127 (callers guarantee x <= 8); x < -125 -> ~0.
-#ifndef TMC_FWD_MAXFREE
-#define TMC_FWD_MAXFREE 0   // forward softmax: optimistic tiles without a maximum scan (exact fallback)
-#endif
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -125.f);
   const float t = x + 12582912.f;            // 1.5 * 2^23: round(x) lands in the low mantissa bits
@@ -245,11 +242,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // The same polynomial on a pair (FADD2 / FFMA2 on packed fp32 pairs, LEA for the exponent add):
 // 12 issue slots per two exponentials instead of ~20.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-#if TMC_FWD_MAXFREE
-  x = make_float2(fminf(fmaxf(x.x, -125.f), 126.f), fminf(fmaxf(x.y, -125.f), 126.f));
-#else
   x = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
-#endif
   const float2 M = make_float2(12582912.f, 12582912.f);
   const float2 t = __fadd2_rn(x, M);
   const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
@@ -800,17 +793,6 @@ __global__ void __launch_bounds__(Geo<D>::THREADS, 1) tc_fwd_kernel(const __grid
           const float2 tt = __fadd2_rn(t01, t23);
           return tt.x + tt.y;
         };
-#if TMC_FWD_MAXFREE
-        // Optimistic tile: sum against the current reference without scanning for the tile maximum.
-        // Any argument above 126 makes the tile sum >= 2^126 (ex2_poly2 clamps there), an argument
-        // that is NaN makes it NaN; both fail the test below and take the exact path.  After the
-        // first reference is set the running sum is >= 1, so terms that underflow are below 2^-126
-        // relative; a reference up to 2^100 below the true maximum costs no fp32 precision.
-        if (mref > -INFINITY) {
-          const float ts = tile_sum(mref);
-          if (ts < 0x1p100f) { sum += ts; continue; }
-        }
-#endif
         const float tmax = tile_max();
         if (tmax > mref + 8.f) {          // lazy rescale: only when the max grows by > 2^8
           sum = (mref == -INFINITY) ? 0.f : sum * ex2(mref - tmax);
@@ -1587,6 +1569,10 @@ struct RowtermArgs {
 };
 
 struct RowtermBatch { RowtermArgs e[kMaxBatch]; int ne; };
+#ifndef TMC_FLUSH_LOG2
+#define TMC_FLUSH_LOG2 -41.f
+#endif
+constexpr float kFlushLog2 = TMC_FLUSH_LOG2;   // log2 of the row-weight flush threshold relative to the scale ws
 
 __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__ RowtermBatch rb_) {
   const RowtermArgs& a = rb_.e[blockIdx.y];
@@ -1611,9 +1597,14 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
     if (r < a.R) {
       const float e = a.ell[(size_t)b * a.R + r], w = a.w[(size_t)b * a.R + r];
       if (w < 0.f) neg = 1;
-      if (e > -INFINITY && w != 0.f) {
+      // P~[r, n] = 2^14 |w[r]|/ws * (pair term / row total) <= 2^14 |w[r]|/ws (1 + rounding): a row
+      // below 2^-41 of the scale has every P~ <= 2^-27, which rounds to zero in both fp16 parts, so
+      // its gradient-GEMM contribution is exactly 0 already; flushing the row (kFlushLog2) also zeroes
+      // its row sum (<= 2^-41 relative) and lets the zero-tile skip drop tiles that carry no fp16 weight.
+      const float lr = (w != 0.f) ? __log2f(fabsf(w)) - lw : -INFINITY;
+      if (e > -INFINITY && lr >= kFlushLog2) {
         const float bt = a.beta ? a.beta[(size_t)b * a.betaStride + r] : 0.f;
-        v = __log2f(fabsf(w)) - lw - (e - bt) * kLog2E;
+        v = lr - (e - bt) * kLog2E;
       }
     }
     a.rterm2[(size_t)b * a.Rpad + r] = v;
