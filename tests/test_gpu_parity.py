@@ -204,6 +204,32 @@ def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw):
                 assert np.array_equal(x, y), (k, i, np.abs(x - y).max())
 
 
+def test_row_weight_flush_is_below_the_bound(torch_cuda):
+    """DESIGN.md R5: the tensor-core reverse pass flushes rows whose upstream weight is below 2^-41
+    of the edge's scale (their P~ is zero in both fp16 parts).  On a C4-shaped tree (sharp
+    posteriors: most parent samples carry no weight) the flushed rows' parameter gradients are
+    exactly 0 on the GPU, the oracle's values there are below 2^-38 of the tensor's largest entry,
+    and the full comparison still meets the 1e-3 bars."""
+    wl = tw.make_workload("C4", B=2, K=260)
+    got = run_gpu(torch_cuda, wl)
+    ref = oracle.estimate_workload(wl)
+    compare(got, ref, tag="flush")
+    flushed = 0
+    for i, pa in enumerate(wl.parent):
+        if pa < 0:
+            continue
+        wpar = np.abs(ref["dlogq"][pa])                       # [B][K_pa]: |dlogp| x marginal of the parent's samples
+        for b in range(wl.B):
+            small = wpar[b] < 2.0 ** -43 * wpar[b].max()
+            if not small.any():
+                continue
+            flushed += int(small.sum())
+            for k in ("dmu", "dlogvar"):
+                assert not got[k][i][b][small].any(), (i, b, k)
+                assert np.abs(ref[k][i][b][small]).max() <= 2.0 ** -38 * np.abs(ref[k][i][b]).max(), (i, b, k)
+    assert flushed > 0
+
+
 @pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=300)), ("C4", dict(B=2, K=200)), ("C2", dict(B=3, K=256)),
                                      ("C0", {}), ("C1", dict(B=4))])
 def test_cuda_graph_replay_matches_eager(torch_cuda, name, kw):
