@@ -862,6 +862,8 @@ struct BwdArgs {
   float *gz, *gmu, *glv;       // gradient outputs [B][M][D]
   float* rowsum;               // [B][M] sum_n P (the edge's column sum) or NULL
   const int *olive, *tlive;    // [B][o_tiles], [B][t_tiles]: 0 = every P~ of the tile is exactly 0 (skipped)
+  int* tflag;                  // row-owner pass: [B][t_tiles] set to 1 when any P~ of a streamed tile is nonzero in fp16
+  const int* oflag;            // column-owner pass: those flags for the owned tiles (0: the tile's sums are 0, R6)
 };
 
 template <int D>
@@ -961,7 +963,9 @@ __host__ __device__ constexpr int bwd_smw(int SG) { return SG == 3 ? 8 : 16; }
 template <int D, int SG>
 __host__ __device__ constexpr int bwd_threads() { return 32 * (bwd_smw(SG) + BGeo<D>::EW + 2 + TMC_BWD_SPLIT); }
 
-template <int D, int GT, int SG>
+// CF: the row-owner pass records which streamed (column) tiles carry fp16 weight (BwdArgs::tflag); the
+// column-owner instantiation (CF = false) has no trace of it in its softmax loop.
+template <int D, int GT, int SG, bool CF>
 __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const __grid_constant__ BwdBatch fb) {
   using G = BGeo<D>;
   constexpr int ST = G::ST, SMW = bwd_smw(SG), EW = G::EW;
@@ -1222,6 +1226,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
 #endif
     // P~ of 32 columns: arguments S + ht + (ho + 14) on packed pairs, ex2, row-sum accumulation,
     // fp16 hi/lo split
+    float pmax = 0.f;   // CF: largest P~ this thread computed in the current streamed tile
     auto chunk_math = [&](const uint32_t* v, float2 hom2, float2* racc, uint32_t* hi, uint32_t* lo) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -1233,6 +1238,10 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         const float2 p23 = poly ? make_float2(ex2_poly(y23.x), ex2_poly(y23.y)) : make_float2(ex2(y23.x), ex2(y23.y));
         racc[0] = __fadd2_rn(racc[0], p01);
         racc[1] = __fadd2_rn(racc[1], p23);
+        if constexpr (CF) {
+          pmax = fmaxf(pmax, fmaxf(p01.x, p01.y));
+          pmax = fmaxf(pmax, fmaxf(p23.x, p23.y));
+        }
         __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
         hi[2 * q] = *reinterpret_cast<uint32_t*>(&h01);
         hi[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h23);
@@ -1267,13 +1276,14 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
     UnitPre nxt = unit_pre(blockIdx.x);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       TMC_BWD_UNIT();
-      (void)b; (void)mt;
+      (void)mt;
       const UnitPre cur = nxt;
       nxt = unit_pre(u + gridDim.x);
       if (!cur.olv) continue;
       const float hom = cur.ho + 14.f;
       const float2 hom2 = make_float2(hom, hom);
       float2 racc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      uint32_t fmask = 0;                // CF: bit j = this thread saw fp16 weight in streamed tile j
       TMC_SMX_MARK(4);
       const uint64_t tm = !a.tlive ? ~0ull : a.t_tiles > 64 ? 0ull
                         : ((uint64_t)__ballot_sync(0xffffffffu, cur.f0) | ((uint64_t)__ballot_sync(0xffffffffu, cur.f1) << 32));
@@ -1284,6 +1294,7 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         TMC_PROF_WAIT(lane == 0, 32 + sw, mbar_wait(&s_full[as], (t / NSB) & 1));
         tc_fence_after();
         TMC_SMX_MARK(0);
+        if constexpr (CF) pmax = 0.f;
         if constexpr (SG == 3) {
           // two column quarters, both TMEM loads in flight before the first wait
           const int cq0 = (sw >> 2) * 2;
@@ -1328,8 +1339,25 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[as]);
+        // Row-owner pass: does this streamed (column) tile carry fp16 weight?  P~ <= 2^-27 everywhere is
+        // a factor 4 below the 2^-25 that rounds to a nonzero fp16, so the column-owner pass's
+        // recomputed P~ of an unflagged tile are zero in both parts whatever its last-bit differences
+        // in S.  NaN counts as weight (fmaxf drops NaN: test the row sums too).  One bit per tile in
+        // a per-thread mask, published once per unit; tiles past 32 (K > 4096) publish at once.
+        if constexpr (CF) {
+          const float rs = (racc[0].x + racc[0].y) + (racc[1].x + racc[1].y);
+          const bool wt = pmax > 0x1p-27f || rs != rs;
+          if (j < 32) fmask |= (uint32_t)wt << j;
+          else if (a.tflag && __any_sync(0xffffffffu, wt) && lane == 0) a.tflag[(size_t)b * a.t_tiles + j] = 1;
+        }
         TMC_SMX_MARK(3);
         ++t;
+      }
+      if constexpr (CF) {
+        if (a.tflag) {   // publish the unit's streamed-tile flags (idempotent stores of 1)
+          const uint32_t m0 = __reduce_or_sync(0xffffffffu, fmask);
+          if ((m0 >> lane) & 1u) a.tflag[(size_t)b * a.t_tiles + lane] = 1;
+        }
       }
       // this warp's row sums -> the epilogue warps
       mbar_wait(&r_empty[ua & 1], ((ua >> 1) & 1) ^ 1);
@@ -1408,7 +1436,10 @@ __global__ void __launch_bounds__(bwd_threads<D, SG>(), 1) tc_bwd_kernel(const _
       TMC_PROF_WAIT(warp == SMW && lane == 0, 10, mbar_wait(&g_full[gb], (ua / GB) & 1));
       tc_fence_after();
       const float sc = a.sgn[b] * (1.f / 16384.f);
-      const float pi = rtot * sc;
+      // R6: an owned tile no P~ of which is nonzero in fp16 carries no weight; its sums are 0 (the
+      // skipping pass never computes it, the dense pass computes exact-zero gradients for it)
+      const bool oz = a.oflag && !a.oflag[(size_t)b * a.o_tiles + mt];
+      const float pi = oz ? 0.f : rtot * sc;
       const bool live = gm < a.M;
       const float* sh = a.shift + (size_t)b * D;
       const size_t row = ((size_t)b * a.M + (live ? gm : 0)) * D;
@@ -1566,6 +1597,8 @@ struct RowtermArgs {
   uint8_t* bx;                   // [B][Rpad/128][kBxBytes]: rterm2 as the bias operand of the column-owner pass
   float* sgn;                    // [B]
   int* live;                     // [B][Rpad/128] 1 if any row of the 128-row tile carries weight
+  int* cflag;                    // [B][ctiles] column-tile fp16-weight flags, zeroed here for the row-owner pass (or NULL)
+  int ctiles;
 };
 
 struct RowtermBatch { RowtermArgs e[kMaxBatch]; int ne; };
@@ -1613,6 +1646,8 @@ __global__ void __launch_bounds__(256) tc_rowterm_kernel(const __grid_constant__
   __syncthreads();
   if (tid == 0) a.sgn[b] = neg ? -ws : ws;
   tile_live_flags(a.rterm2 + (size_t)b * a.Rpad, a.Rpad / kTileRows, a.live + (size_t)b * (a.Rpad / kTileRows));
+  if (a.cflag)
+    for (int t = tid; t < a.ctiles; t += 256) a.cflag[(size_t)b * a.ctiles + t] = 0;
 }
 
 }  // namespace tc
@@ -1630,7 +1665,7 @@ constexpr int kBwdGroups = 3;
 struct TcLatentBuf {
   bool ok = false;          // this latent's (non-root) edge runs on tensor cores
   int D = 0, KzPad = 0, KpPad = 0;
-  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, rbx = 0, sgn = 0, rlive = 0, clive = 0;
+  size_t xt = 0, yt = 0, beta = 0, cb2 = 0, bx = 0, shift = 0, rterm2 = 0, rbx = 0, sgn = 0, rlive = 0, clive = 0, clive2 = 0;
   bool bwd_ok = false;      // reverse pass on tensor cores
 };
 
@@ -1677,6 +1712,7 @@ inline void tc_plan(const std::vector<int>& parent, const std::vector<int>& K, c
     t.rbx = tc_carve(cur, Bn * (Rpad / 128) * tc::kBxBytes);
     t.rlive = tc_carve(cur, Bn * (Rpad / 128) * 4);
     t.clive = tc_carve(cur, Bn * (Cpad / 128) * 4);
+    t.clive2 = tc_carve(cur, Bn * (Cpad / 128) * 4);
     t.sgn = tc_carve(cur, Bn * 4);
     t.bwd_ok = true;
   }
@@ -1809,21 +1845,24 @@ inline int tc_pass_forward(const PassArgs& a, const TcLatentBuf& t, void* ws, bo
   return tc_pass_forward_batch(&a, &tp, 1, ws, zrows, s);
 }
 
-template <int D, int GT, int SG>
+template <int D, int GT, int SG, bool CF>
 inline void tc_bwd_launch_t(const tc::BwdBatch& fb, cudaStream_t s) {
   using G = tc::BGeo<D>;
   static bool attr[kMaxDevices] = {};
-  ensure_smem_attr(tc::tc_bwd_kernel<D, GT, SG>, (int)G::SMEM, attr);
+  ensure_smem_attr(tc::tc_bwd_kernel<D, GT, SG, CF>, (int)G::SMEM, attr);
   const int sms = sm_count();
   const int units = fb.ustart[fb.ne];
   const int grid = units < sms ? units : sms;
-  if (grid > 0) tc::tc_bwd_kernel<D, GT, SG><<<grid, tc::bwd_threads<D, SG>(), G::SMEM, s>>>(fb);
+  if (grid > 0) tc::tc_bwd_kernel<D, GT, SG, CF><<<grid, tc::bwd_threads<D, SG>(), G::SMEM, s>>>(fb);
 }
 
 template <int D>
-inline void tc_bwd_launch(const tc::BwdBatch& fb, cudaStream_t s) {
-  tc_bwd_launch_t<D, kGradTerms, kBwdGroups>(fb, s);
+inline void tc_bwd_launch(const tc::BwdBatch& fb, bool colflags, cudaStream_t s) {
+  if (colflags) tc_bwd_launch_t<D, kGradTerms, kBwdGroups, true>(fb, s);
+  else tc_bwd_launch_t<D, kGradTerms, kBwdGroups, false>(fb, s);
 }
+
+constexpr int kColFlagMaxTiles = 8;   // column-tile weight flags (R6) for edges with K_column <= 1024
 
 inline bool tc_bwd_edge_ok(const TcLatentBuf& t, const PassArgs& a) { return t.ok && t.bwd_ok && !a.pair; }
 
@@ -1838,6 +1877,14 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
     tc::BwdBatch fb{};
     tc::RowtermBatch rtb{};
     fb.ne = std::min(tc::kMaxBatch, ne - e0);
+    // Column-tile weight flags (reading R6) for batches whose edges have at most kColFlagMaxTiles
+    // column tiles: recording them costs the row-owner pass ~2% where it is tensor-bound (K = 2048,
+    // where it also found nothing more to skip) and nothing where the per-unit latency binds.
+    bool colflags = true;
+    for (int k = 0; k < fb.ne; ++k) {
+      const TcLatentBuf& t = *ts[e0 + k];
+      if ((zrows ? t.KpPad : t.KzPad) / 128 > kColFlagMaxTiles) colflags = false;
+    }
     rtb.ne = fb.ne;
     fb.ustart[0] = 0;
     for (int k = 0; k < fb.ne; ++k) {
@@ -1854,6 +1901,8 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
         r.rterm2 = rterm2; r.sgn = sgn;
         r.bx = w + t.rbx;
         r.live = reinterpret_cast<int*>(w + t.rlive);
+        r.cflag = reinterpret_cast<int*>(w + t.clive2);
+        r.ctiles = Cpad / 128;
       }
       tc::BwdArgs& f = fb.e[k];
       const bool own_rows = (mode == 1);
@@ -1877,10 +1926,15 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
       f.shift = reinterpret_cast<const float*>(w + t.shift);
       f.gz = a.gz; f.gmu = a.gmu; f.glv = a.glv;
       f.rowsum = own_rows ? nullptr : a.colsum;
+      // Column tiles: the exact flags of the forward (a message of -inf) for the row-owner pass, which
+      // records the tiles that carry fp16 weight (clive2); the column-owner pass owns only those.
+      int* cl2 = reinterpret_cast<int*>(w + t.clive2);
+      f.tflag = (own_rows && colflags) ? cl2 : nullptr;
+      f.oflag = (!own_rows && colflags) ? cl2 : nullptr;
       if (!dense_reverse) {
         const int* rl = reinterpret_cast<const int*>(w + t.rlive);
         const int* cl = reinterpret_cast<const int*>(w + t.clive);
-        f.olive = own_rows ? rl : cl;
+        f.olive = own_rows ? rl : (colflags ? cl2 : cl);
         f.tlive = own_rows ? cl : rl;
       }
       f.alpha = a.alpha;
@@ -1896,8 +1950,8 @@ inline int tc_pass_backward_batch(const PassArgs* as, const TcLatentBuf* const* 
     // gradient GEMM (K = 128 streamed rows, N = 2D): (12 D + 32 + 12 D) flops per pair
     fb.flops_per_tile = (unsigned long long)((12 + 4 * (kGradTerms > 3 ? 2 : kGradTerms)) * ts[e0]->D + 32) * 128 * 128;
     ProfScope ps(PF_TC_BWD, s);
-    if (ts[e0]->D == 32) tc_bwd_launch<32>(fb, s);
-    else tc_bwd_launch<64>(fb, s);
+    if (ts[e0]->D == 32) tc_bwd_launch<32>(fb, mode == 1 && colflags, s);
+    else tc_bwd_launch<64>(fb, mode == 1 && colflags, s);
     ++launched;
   }
   return launched;

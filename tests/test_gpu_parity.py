@@ -205,8 +205,9 @@ def test_reverse_zero_tile_skip_is_exact(torch_cuda, name, kw):
 
 
 def test_row_weight_flush_is_below_the_bound(torch_cuda):
-    """DESIGN.md R5: the tensor-core reverse pass flushes rows whose upstream weight is below 2^-41
-    of the edge's scale (their P~ is zero in both fp16 parts).  On a C4-shaped tree (sharp
+    """DESIGN.md R5/R6: the tensor-core reverse pass flushes rows whose upstream weight is below 2^-41
+    of the edge's scale (their P~ is zero in both fp16 parts) and does not own column tiles that
+    carry no fp16 weight.  On a C4-shaped tree (sharp
     posteriors: most parent samples carry no weight) the flushed rows' parameter gradients are
     exactly 0 on the GPU, the oracle's values there are below 2^-38 of the tensor's largest entry,
     and the full comparison still meets the 1e-3 bars."""
@@ -228,6 +229,24 @@ def test_row_weight_flush_is_below_the_bound(torch_cuda):
                 assert not got[k][i][b][small].any(), (i, b, k)
                 assert np.abs(ref[k][i][b][small]).max() <= 2.0 ** -38 * np.abs(ref[k][i][b]).max(), (i, b, k)
     assert flushed > 0
+    # R6: a column tile (128 consecutive samples of the child) none of whose pair terms is nonzero in
+    # fp16 is not owned by the column-owner pass: dz and dlogq of its samples are exactly 0.  A tile
+    # whose marginals are all below 2^-52 of the latent's largest has every pair term below
+    # 2^-52 K ws <= 2^-43 ws, i.e. P~ < 2^-29, under the 2^-27 flag threshold.
+    dead = 0
+    for i, pa in enumerate(wl.parent):
+        if pa < 0:
+            continue
+        pi = np.abs(ref["dlogq"][i])
+        for b in range(wl.B):
+            for t0 in range(0, wl.K[i], 128):
+                sl = slice(t0, min(wl.K[i], t0 + 128))
+                if pi[b, sl].max() >= 2.0 ** -52 * pi[b].max():
+                    continue
+                dead += 1
+                assert not got["dz"][i][b][sl].any() and not got["dlogq"][i][b][sl].any(), (i, b, t0)
+                assert np.abs(ref["dz"][i][b][sl]).max() <= 2.0 ** -38 * np.abs(ref["dz"][i][b]).max(), (i, b, t0)
+    assert dead > 0
 
 
 @pytest.mark.parametrize("name,kw", [("C3", dict(B=3, K=300)), ("C4", dict(B=2, K=200)), ("C2", dict(B=3, K=256)),
