@@ -602,6 +602,17 @@ def test_large_K_single_datapoint(torch_cuda):
     compare(got, ref, tag="K8192")
 
 
+def test_K_beyond_64_tiles(torch_cuda):
+    """K = 8320 (65 tiles per side): past the 64-bit live-tile masks of the reverse pass, whose
+    roles fall back to per-tile flag loads, and past the fixed-size flag arrays round 1 had in the
+    column-bias and row-term kernels.  One datapoint carries dlogp = 0 (all tiles dead)."""
+    wl = tw.make_workload("C3", B=2, K=8320, parent=[-1, 0, 1], D=[32] * 3)
+    w = np.array([1.0, 0.0])
+    got = run_gpu(torch_cuda, wl, dlogp=w)
+    ref = oracle.estimate_workload(wl, dlogp=w)
+    compare(got, ref, tag="K8320")
+
+
 def test_empty_batch_launches_nothing(torch_cuda):
     import paper_1806_08593_b200 as tmc
     torch = torch_cuda
