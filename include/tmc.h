@@ -88,7 +88,11 @@ typedef enum {
 enum {
   TMC_FLAG_VALIDATE = 1u,      /* scan every input for NaN/+inf first (TMC_ERR_NONFINITE), synchronous   */
   TMC_FLAG_DENSE_REVERSE = 2u, /* reverse pass computes every tile, including tiles whose pair weights  */
-                               /* are all exactly 0 (skipped by default; identical results, measurement) */
+                               /* are all exactly 0 (skipped by default; identical results, measurement). */
+                               /* On the tensor-core path "weight 0" includes pair terms that are zero in */
+                               /* both fp16 parts of their weight (below 2^-41 of the edge's largest      */
+                               /* upstream weight, R5/R6): their rows and column sums are 0 in  */
+                               /* both modes, so the two stay bit-identical                               */
   TMC_FLAG_TWO_PASS_REVERSE = 4u, /* tensor-core reverse pass as two owner passes (S and P~ recomputed   */
                                /* per orientation); equal to the single pass within fp32 rounding        */
   TMC_FLAG_SINGLE_PASS_REVERSE = 8u /* tensor-core reverse pass as one pass (one S and P~ per tile, D = 32 */
